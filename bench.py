@@ -1,0 +1,402 @@
+#!/usr/bin/env python
+"""HRKAN PINN loss+grad step benchmark (BASELINE.json metric: collocation points/s per PINN
+loss+grad step, fp32, and % of the FP32/tensor peak).
+
+A step = one pass of the whole hot path over the synthetic collocation set of the workload:
+hrkan_pinn_loss_grad (forward jet, residual, loss, reverse pass) + the data-parallel allreduce of
+the flat [dL/dtheta | loss parts | flag] buffer (N > 1) + hrkan_adam_step.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C5] [--impl ours|reference]
+
+N > 1 is launched by torchrun (one process per GPU, NCCL).  Points are sharded in contiguous blocks
+(strong scaling: the global set of the config is fixed, every rank gets 1/N of it).
+Rank 0 prints ONE JSON line.  See DESIGN.md "Measurement" for every field.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import hrkan_inputs as HI  # noqa: E402
+
+METRIC = "collocation points/s per PINN loss+grad step (fp32)"
+UNIT = "points/s"
+DEFAULT_CONFIG = "C5"
+
+
+def peaks():
+    """Roofline denominators: MEASURED_PEAKS.json (driver-written) else the profiling guide fallback."""
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return {"bf16": d.get("bf16_tflops", 1619.2), "bf16_sustained": d.get("bf16_tflops_sustained", 1350.0),
+                "hbm": d.get("hbm_gbs", 6545.6), "sm_max_mhz": d.get("sm_max_mhz", 1965.0), "source": "measured"}
+    return {"bf16": 1590.0, "bf16_sustained": 1400.0, "hbm": 6650.0, "sm_max_mhz": 1965.0, "source": "fallback"}
+
+
+# ------------------------------------------------------------------------------------------
+# Algorithmic FLOPs per kernel class (the dense KAN matrix product over all B
+# bases; the first layer is structured: 2*O*D*B + (C-1)*2*O*B per point).
+# ------------------------------------------------------------------------------------------
+def class_flops(w: HI.Workload, n_int: int, n_bi: int, c_int: int):
+    B = w.B
+    L = len(w.widths) - 1
+    out = {}
+    for l in range(L):
+        I, O = w.widths[l], w.widths[l + 1]
+        kind = "first" if l == 0 else ("last" if l == L - 1 else "hidden")
+        for cls in ("fwd", "wgrad", "dgrad"):
+            if cls == "dgrad" and l == 0:
+                continue
+            tot = 0
+            for n, C in ((n_int, c_int), (n_bi, 1)):
+                if l == 0:
+                    per = 2 * O * w.D * B + (C - 1) * 2 * O * B
+                else:
+                    per = 2 * C * O * I * B
+                tot += n * per
+            key = f"{cls}_{kind}"
+            out[key] = out.get(key, 0) + tot
+    return out
+
+
+def interior_channels(w: HI.Workload) -> int:
+    return 1 + 2 + 1 if w.pde == "burgers" else 1 + 2 * w.D
+
+
+# ------------------------------------------------------------------------------------------
+# clocks during the timed region (nvidia-smi sampler)
+# ------------------------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in self.lines:
+            parts = [p.strip() for p in l.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------------------
+# CPU oracle (cpu_baseline and --impl reference)
+# ------------------------------------------------------------------------------------------
+def _blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        n = [i.get("num_threads", 1) for i in threadpool_info() if i.get("user_api") == "blas"]
+        return max(n) if n else 1
+    except Exception:
+        return len(os.sched_getaffinity(0))
+
+
+def oracle_sample(w: HI.Workload, ps: HI.PointSet, n_int: int):
+    """A strided sample of the workload with n_int interior points and a proportional share of
+    boundary/initial points (at least 1 each)."""
+    s_int = max(1, len(ps.interior) // n_int)
+    frac = (len(ps.interior) // s_int) / len(ps.interior)
+    nb = max(1, int(round(ps.n_bi * frac)))
+    s_bi = max(1, ps.n_bi // nb)
+    return ps.subset(s_int, s_bi)
+
+
+def time_oracle(w: HI.Workload, ps: HI.PointSet, target_s: float):
+    """Time the float64 oracle loss+grad on a bounded sample sized for ~target_s seconds.
+    Returns (points/s, sample description, seconds)."""
+    from oracle import hrkan_oracle as O
+    net = O.Net(w.widths, w.G, w.k, w.m, w.lo, w.hi)
+    params = HI.random_params(w.widths, w.G, w.k, seed=HI.PARAM_SEED)
+    pde = {"kind": w.pde, "alpha": w.alpha, "adv": w.adv, "visc": w.visc}
+
+    def run(sample):
+        bi = sample.boundary if sample.initial is None else np.concatenate([sample.boundary, sample.initial])
+        gbi = sample.g_boundary if sample.initial is None else np.concatenate([sample.g_boundary, sample.g_initial])
+        t0 = time.perf_counter()
+        O.loss_grad(net, params, pde, sample.interior, bi, gbi)
+        return time.perf_counter() - t0, len(sample.interior) + len(bi)
+
+    n = 16
+    dt, npts = run(oracle_sample(w, ps, n))
+    while dt < target_s / 8 and n < len(ps.interior):
+        n = min(len(ps.interior), int(n * max(2.0, min(16.0, (target_s / 4) / max(dt, 1e-3)))))
+        dt, npts = run(oracle_sample(w, ps, n))
+    sample = oracle_sample(w, ps, n)
+    desc = (f"{w.key} strided sample: {len(sample.interior)} interior + {sample.n_bi} boundary/initial points "
+            f"of the same synthetic set, float64 numpy oracle loss+grad")
+    return npts / dt, desc, dt, npts
+
+
+# ------------------------------------------------------------------------------------------
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default=os.environ.get("HRKAN_BENCH_CONFIG", DEFAULT_CONFIG))
+    ap.add_argument("--m", type=int, default=None, help="override the HR order (C4 sweep)")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--engine", type=int, default=0, help="0 auto, 1 SIMT only, 2 tensor cores")
+    ap.add_argument("--chunk", type=int, default=0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+def workload(args) -> HI.Workload:
+    w = HI.WORKLOADS[args.config]
+    if args.m is not None:
+        w = w.with_m(args.m)
+    return w
+
+
+def run_reference(args):
+    """The reference arm for this tier = the float64 oracle as it stands, on the host cores, on a
+    bounded strided sample of the same workload (rank 0 only; other ranks exit without work)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import hrkan_oracle as O
+    w = workload(args)
+    ps = HI.make_points(w)
+    per_step = max(1.0, 120.0 / max(1, args.steps + args.warmup))
+    _, desc, _, _ = time_oracle(w, ps, per_step)
+    n = int(desc.split("sample: ")[1].split(" interior")[0])
+    sample = oracle_sample(w, ps, n)
+    net = O.Net(w.widths, w.G, w.k, w.m, w.lo, w.hi)
+    params = HI.random_params(w.widths, w.G, w.k, seed=HI.PARAM_SEED)
+    pde = {"kind": w.pde, "alpha": w.alpha, "adv": w.adv, "visc": w.visc}
+    bi = sample.boundary if sample.initial is None else np.concatenate([sample.boundary, sample.initial])
+    gbi = sample.g_boundary if sample.initial is None else np.concatenate([sample.g_boundary, sample.g_initial])
+    npts = len(sample.interior) + len(bi)
+    times = []
+    for s in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        O.loss_grad(net, params, pde, sample.interior, bi, gbi)
+        if s >= args.warmup:
+            times.append(time.perf_counter() - t0)
+    value = npts * len(times) / sum(times)
+    cores = _blas_threads()
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * sum(times) / len(times),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": w.key, "name": w.name, "sample": desc},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    import __graft_entry__
+    __graft_entry__.build()
+    from paper_2409_14248_b200 import HRKANNet, pde_struct
+    from paper_2409_14248_b200.hrkan import KERNEL_CLASSES
+
+    w = workload(args)
+    ps = HI.make_points(w)
+    sh = ps.shard(rank, world)
+    n_int_g, n_bi_g = len(ps.interior), ps.n_bi
+    dev = torch.device(f"cuda:{local}")
+    cu = lambda a: None if a is None else torch.from_numpy(a).to(dev)
+    d_int, d_bnd, d_gb, d_ini, d_gi = cu(sh.interior), cu(sh.boundary), cu(sh.g_boundary), cu(sh.initial), cu(sh.g_initial)
+    net = HRKANNet(w.widths, w.G, w.k, w.m, seed=HI.PARAM_SEED, device=local)
+    net.set_engine(args.engine)
+    if args.chunk:
+        net.set_chunk_points(args.chunk)
+    npar = net.n_params
+    pde = pde_struct(w.pde, w.alpha, w.adv, w.visc)
+    out = torch.empty(npar + 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step(i_int, i_bnd, i_gb, i_ini, i_gi, res=None):
+        net.pinn_loss_grad(pde, i_int, i_bnd, i_gb, i_ini, i_gi, n_int_global=n_int_g, n_bi_global=n_bi_g, out=out)
+        if world > 1:
+            dist.all_reduce(out, op=dist.ReduceOp.SUM)
+        net.adam_step(out[:npar])
+        if res is not None:
+            res.copy_(out[npar:npar + 4], non_blocking=True)
+
+    # warm-up (first warm-up step profiled per kernel class to find the dominant kernel)
+    net.profile_enable(True)
+    for s in range(args.warmup):
+        step(d_int, d_bnd, d_gb, d_ini, d_gi)
+        if s == 0:
+            torch.cuda.synchronize()
+            prof0 = net.profile_read()
+            net.profile_enable(False)
+    torch.cuda.synchronize()
+    dominant = max(prof0, key=lambda k: prof0[k][0])
+
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # > 126 MB L2
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    net.profile_enable(True)            # live per-launch events for the kernel classes, same stream
+    net.profile_read()
+    launches0 = net.launch_count()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for s in range(args.steps):
+            flush.fill_(float(s))        # L2 flush between timed steps (outside the event pair)
+            ev[s][0].record(stream)
+            step(d_int, d_bnd, d_gb, d_ini, d_gi)
+            ev[s][1].record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    launches = net.launch_count() - launches0
+    prof = net.profile_read()
+    net.profile_enable(False)
+    ms = sum(a.elapsed_time(b) for a, b in ev) / args.steps
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    n_points = n_int_g + n_bi_g
+    value = n_points / (ms_max / 1000.0)
+    loss = out[npar:npar + 2].sum().item()
+    flag = out[npar + 2].item()
+
+    # ---------------- end to end: HOST (pinned) inputs through the C ABI, result read back
+    e2e = None
+    if not args.no_e2e:
+        pin = lambda a: None if a is None else torch.from_numpy(a).pin_memory()
+        h = [pin(sh.interior), pin(sh.boundary), pin(sh.g_boundary), pin(sh.initial), pin(sh.g_initial)]
+        res = torch.empty(4, dtype=torch.float32).pin_memory()
+        h2d = sum(x.numel() * 4 for x in h if x is not None)
+        step(*h, res=res)
+        torch.cuda.synchronize()
+        e_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        for s in range(args.steps):
+            flush.fill_(float(s))
+            e_ev[s][0].record(stream)
+            step(*h, res=res)
+            e_ev[s][1].record(stream)
+        torch.cuda.synchronize()
+        ems = sum(a.elapsed_time(b) for a, b in e_ev) / args.steps
+        te = torch.tensor([ems], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": n_points / (float(te.item()) / 1000.0), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": 16, "ms_per_step": float(te.item())}
+
+    # ---------------- roofline of the dominant kernel class (live CUDA events, same stream)
+    pk = peaks()
+    c_int = interior_channels(w)
+    fl = class_flops(w, len(sh.interior), sh.n_bi, c_int)
+    dom_ms, dom_n = prof[dominant]
+    dom_flops = fl.get(dominant, 0) * args.steps
+    step_ms_local = ms
+    share = (dom_ms / args.steps) / step_ms_local if step_ms_local > 0 else None
+    clock_mhz = pk["sm_max_mhz"]
+    # SIMT (FFMA) peak = 148 SMs x 128 FP32 lanes x 2 flop x SM clock; TF32 tensor = bf16 x (1.1/2.25)
+    n_sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    fp32_peak = n_sms * 128 * 2 * clock_mhz * 1e6 / 1e12
+    tf32_peak = pk["bf16_sustained"] * (1.1 / 2.25)
+    engine = os.environ.get("HRKAN_ROOFLINE_BOUND", "alu")
+    achieved = dom_flops / (dom_ms / 1000.0) / 1e12 if dom_ms > 0 else 0.0
+    if engine == "tensor":
+        peak, bound = tf32_peak, "tensor"
+    else:
+        peak, bound = fp32_peak, "alu"
+    roofline = {"kernel_class": dominant, "bound": bound, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": achieved / peak if peak else None, "traffic": None,
+                "launches": dom_n, "avg_launch_ms": dom_ms / max(1, dom_n), "share_of_step": share,
+                "algorithmic_flops_per_step": fl.get(dominant, 0),
+                "peak_note": (f"FP32 FFMA = {n_sms} SMs x 128 lanes x 2 x {clock_mhz:.0f} MHz (derived)" if bound == "alu"
+                              else f"TF32 = bf16 sustained {pk['bf16_sustained']} x 1.1/2.25 ({pk['source']})"),
+                "per_class_ms_per_step": {k: v[0] / args.steps for k, v in prof.items() if v[1]}}
+
+    if rank == 0:
+        cpu = None
+        if not args.no_cpu_baseline and world == 1:
+            pps, desc, dt, npts = time_oracle(w, ps, args.cpu_seconds)
+            cpu = {"value": pps, "unit": UNIT, "cores": _blas_threads(), "kind": "oracle", "sample": desc,
+                   "seconds": dt}
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": {"workload": w.key, "name": w.name, "n_interior": n_int_g, "n_boundary_initial": n_bi_g,
+                           "widths": list(w.widths), "G": w.G, "k": w.k, "m": w.m, "pde": w.pde,
+                           "parallelism": f"dp{world}", "l2": "flushed between timed steps (256 MiB write)",
+                           "engine": args.engine},
+                "e2e": e2e, "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpu,
+                "clocks": clk.summary(), "loss": loss, "nonfinite_flag": flag,
+                "step": "pinn_loss_grad + allreduce(N>1) + adam_step"}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,9 @@
+"""B200-native (sm_100a) HRKAN physics-informed loss + gradient hot path (arXiv 2409.14248).
+
+`hrkan`    ctypes binding of libhrkan.so (include/hrkan.h): create / forward_jet /
+           pinn_loss_grad / adam_step / free.
+`parallel` data-parallel step: contiguous point shards per rank, global normalisers and ONE
+           allreduce of the flat [dL/dtheta | loss parts | flag] buffer (torch.distributed,
+           NCCL on GPUs, gloo in the CPU tests).
+"""
+from .hrkan import HRKANNet, HrkanError, HrkanPde, load_library, pde_struct  # noqa: F401

@@ -1,0 +1,690 @@
+// hrkan_abi.cu -- libhrkan.so: the C ABI of include/hrkan.h, the network object, the chunked
+// scheduler of the loss+gradient step and the host->device staging of host buffers.
+//
+// Every arithmetic step of the hot path runs in the kernels of simt_kernels.cuh / tc_kernels.cuh;
+// this file only validates arguments, owns device memory and sequences launches on the caller's
+// stream (SURVEY §3 "New build" call stack).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <type_traits>
+#include <vector>
+
+#include "../../include/hrkan.h"
+#include "simt_kernels.cuh"
+
+using namespace hrkan;
+
+namespace {
+
+thread_local std::string g_err;
+
+hrkan_status fail(hrkan_status s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+
+#define HR_CUDA(call)                                                                         \
+  do {                                                                                        \
+    cudaError_t e_ = (call);                                                                  \
+    if (e_ != cudaSuccess)                                                                    \
+      return fail(HRKAN_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_));          \
+  } while (0)
+
+#define HR_TRY(...)                     \
+  do {                                  \
+    hrkan_status s_ = (__VA_ARGS__);    \
+    if (s_ != HRKAN_OK) return s_;      \
+  } while (0)
+
+template <int V>
+using IC = std::integral_constant<int, V>;
+
+// RAII current-device switch (the caller's current device is restored).
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+bool is_device_ptr(const void* p) {
+  if (!p) return true;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  cudaError_t ensure(size_t n) {
+    if (n <= bytes) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    cudaError_t e = cudaMalloc(&p, n);
+    if (e == cudaSuccess) bytes = n;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  float* f() const { return static_cast<float*>(p); }
+};
+
+}  // namespace
+
+struct hrkan_net {
+  int device = 0;
+  int L = 0, D = 0, G = 0, k = 0, m = 0, B = 0;
+  float lo = -1.f, hi = 1.f;
+  std::vector<int> widths;
+  std::vector<int64_t> w_off, b_off;   // offsets into the flat parameter vector
+  int64_t n_params = 0;
+  int64_t max_layer_w = 0;
+  int max_width = 0;                   // max over widths[1..L]
+  BasisCfg bc{};
+  float* params = nullptr;             // flat, owned
+  float* adam_m = nullptr;
+  float* adam_v = nullptr;
+  int64_t adam_t = 0;
+  std::vector<float*> wt;              // derived: W_l transposed to [I][B][O]
+  bool derived_dirty = true;
+  int64_t chunk = 0;                   // 0 = auto
+  int engine = 0;
+  int64_t launches = 0;
+  int num_sms = 148;
+  // workspace
+  DevBuf jets, adj_a, adj_b, loss_part, w_part, b_part;
+  DevBuf st_int, st_f, st_bnd, st_gb, st_ini, st_gi, st_out, st_pts, st_u, st_du, st_d2u;
+  DevBuf tc_ws;                         // tensor-core path scratch (split weights, hi/lo jets)
+  // device-time profiling (hrkan_profile_enable / hrkan_profile_read)
+  struct ProfEv { cudaEvent_t a, b; int cls; };
+  bool prof_on = false;
+  std::vector<ProfEv> prof_pool;
+  size_t prof_used = 0;
+};
+
+#include "tc_kernels.cuh"   // tensor-core (tcgen05) hidden-layer engine; needs hrkan_net
+
+namespace {
+
+constexpr int NZ_MAX = 64;
+
+int prof_pre(hrkan_net* net, cudaStream_t st) {
+  if (!net->prof_on) return -1;
+  if (net->prof_used == net->prof_pool.size()) {
+    hrkan_net::ProfEv ev{};
+    if (cudaEventCreate(&ev.a) != cudaSuccess || cudaEventCreate(&ev.b) != cudaSuccess) return -1;
+    net->prof_pool.push_back(ev);
+  }
+  cudaEventRecord(net->prof_pool[net->prof_used].a, st);
+  return (int)net->prof_used++;
+}
+
+hrkan_status check_launch(hrkan_net* net, const char* what, int cls = HRKAN_K_OTHER, cudaStream_t st = nullptr,
+                          int prof_idx = -1) {
+  net->launches++;
+  cudaError_t e = cudaGetLastError();
+  if (prof_idx >= 0) {
+    cudaEventRecord(net->prof_pool[prof_idx].b, st);
+    net->prof_pool[prof_idx].cls = cls;
+  }
+  if (e != cudaSuccess) return fail(HRKAN_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  return HRKAN_OK;
+}
+
+// Launch statement bracketed by profiling events and followed by the launch-error check.
+#define HR_LAUNCH(CLS, NAME, ...)                                   \
+  do {                                                              \
+    const int pi_ = prof_pre(net, st);                              \
+    __VA_ARGS__;                                                    \
+    HR_TRY(check_launch(net, NAME, CLS, st, pi_));                  \
+  } while (0)
+
+int64_t auto_chunk(const hrkan_net* net) {
+  if (net->chunk > 0) return net->chunk;
+  const int C = 1 + 2 * net->D;
+  int64_t sumw = 0;
+  for (int l = 1; l <= net->L; ++l) sumw += net->widths[l];
+  const double bytes_per_point = 4.0 * C * (double)(sumw + 2 * net->max_width) * 1.0;
+  const double budget = 12.0e9;
+  int64_t c = (int64_t)(budget / bytes_per_point);
+  c = std::min<int64_t>(c, 1 << 20);
+  c = std::max<int64_t>(256, c / 256 * 256);
+  return c;
+}
+
+// Workspace for chunks of Pc points with C channels.
+hrkan_status ensure_workspace(hrkan_net* net, int64_t Pc, int C) {
+  int64_t sumw = 0;
+  for (int l = 1; l <= net->L; ++l) sumw += net->widths[l];
+  HR_CUDA(net->jets.ensure(sizeof(float) * (size_t)Pc * C * sumw));
+  HR_CUDA(net->adj_a.ensure(sizeof(float) * (size_t)Pc * C * net->max_width));
+  HR_CUDA(net->adj_b.ensure(sizeof(float) * (size_t)Pc * C * net->max_width));
+  HR_CUDA(net->loss_part.ensure(sizeof(float) * 2 * (size_t)((Pc + 255) / 256 + 1)));
+  HR_CUDA(net->w_part.ensure(sizeof(float) * (size_t)NZ_MAX * net->max_layer_w));
+  HR_CUDA(net->b_part.ensure(sizeof(float) * (size_t)NZ_MAX * net->max_width));
+  return HRKAN_OK;
+}
+
+hrkan_status refresh_derived(hrkan_net* net, cudaStream_t st) {
+  if (!net->derived_dirty) return HRKAN_OK;
+  for (int l = 0; l < net->L; ++l) {
+    const int I = net->widths[l], O = net->widths[l + 1];
+    const int64_t n = (int64_t)O * I * net->B;
+    HR_LAUNCH(HRKAN_K_OTHER, "k_transpose_w",
+              k_transpose_w<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(net->params + net->w_off[l], net->wt[l], O, I * net->B));
+  }
+  HR_TRY(tc_refresh_weights(net, st));
+  net->derived_dirty = false;
+  return HRKAN_OK;
+}
+
+// Stage a host input (n floats) into `buf`, or pass a device pointer through.
+hrkan_status stage_in(const float* src, int64_t n, DevBuf& buf, cudaStream_t st, const float** out) {
+  if (!src || n == 0 || is_device_ptr(src)) {
+    *out = src;
+    return HRKAN_OK;
+  }
+  HR_CUDA(buf.ensure(sizeof(float) * (size_t)n));
+  HR_CUDA(cudaMemcpyAsync(buf.p, src, sizeof(float) * (size_t)n, cudaMemcpyHostToDevice, st));
+  *out = buf.f();
+  return HRKAN_OK;
+}
+
+template <class F>
+hrkan_status with_m(int m, F&& f) {
+  switch (m) {
+    case 2: return f(IC<2>{});
+    case 3: return f(IC<3>{});
+    case 4: return f(IC<4>{});
+    case 5: return f(IC<5>{});
+    case 6: return f(IC<6>{});
+    case 7: return f(IC<7>{});
+    case 8: return f(IC<8>{});
+  }
+  return fail(HRKAN_EINVAL, "m must be in [2, 8]");
+}
+
+enum PassKind { PASS_JET = 0, PASS_INTERIOR = 1, PASS_BOUNDARY = 2 };
+
+struct PassArgs {
+  PassKind kind;
+  const float* pts;        // [P][D] device
+  int64_t P;
+  const float* forcing;    // interior Poisson (device) or null
+  const float* g;          // boundary targets (device)
+  float* u; float* du; float* d2u;   // PASS_JET outputs (device)
+  float* grad;             // flat gradient (device)
+  float* out_loss;         // device scalar slot
+  float* out_flag;
+  const hrkan_pde* pde;
+  float inv_n;             // 1/N_int_global or 1/N_bi_global
+};
+
+// Forward + (optional) loss/seeds + reverse over one point set, chunk by chunk.
+template <int NF, int NS, int M>
+hrkan_status run_pass(hrkan_net* net, const PassArgs& a, cudaStream_t st) {
+  constexpr int C = 1 + NF + NS;
+  const int L = net->L, D = net->D;
+  const int64_t Pc = std::min<int64_t>(auto_chunk(net), std::max<int64_t>(a.P, 1));
+  HR_TRY(ensure_workspace(net, Pc, C));
+  // layer-input jet buffers: jet[l] for l = 1..L (jet[L] = network output [P][C][1])
+  std::vector<float*> jet(L + 1, nullptr);
+  {
+    float* q = net->jets.f();
+    for (int l = 1; l <= L; ++l) {
+      jet[l] = q;
+      q += (size_t)Pc * C * net->widths[l];
+    }
+  }
+  const BasisCfg bc = net->bc;
+  for (int64_t c0 = 0; c0 < a.P; c0 += Pc) {
+    const int64_t n = std::min(Pc, a.P - c0);
+    const float* X0 = a.pts + c0 * D;
+    // ---------------- forward (SURVEY §8(a) a1, a2, a3/a8 value part)
+    for (int l = 0; l < L; ++l) {
+      const int I = net->widths[l], O = net->widths[l + 1];
+      const float* in = (l == 0) ? X0 : jet[l];
+      bool done = false;
+      if (l > 0) HR_TRY(tc_forward_layer<NF, NS, M>(net, l, in, jet[l + 1], n, st, &done));
+      if (!done) {
+        const int64_t tot = n * O;
+        const unsigned grid = (unsigned)((tot + 255) / 256);
+        const int cls = (l == 0) ? HRKAN_K_FWD_FIRST : (l == L - 1 ? HRKAN_K_FWD_LAST : HRKAN_K_FWD_HIDDEN);
+        if (l == 0)
+          HR_LAUNCH(cls, "k_fwd_simt", k_fwd_simt<NF, NS, M, true><<<grid, 256, 0, st>>>(in, net->wt[l], net->params + net->b_off[l], jet[l + 1], n, I, O, bc));
+        else
+          HR_LAUNCH(cls, "k_fwd_simt", k_fwd_simt<NF, NS, M, false><<<grid, 256, 0, st>>>(in, net->wt[l], net->params + net->b_off[l], jet[l + 1], n, I, O, bc));
+      }
+    }
+    if (a.kind == PASS_JET) {
+      if constexpr (NF == NS && NF >= 1) {
+        HR_LAUNCH(HRKAN_K_OTHER, "k_scatter_jet",
+                  k_scatter_jet<NF><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(jet[L], n, a.u ? a.u + c0 : nullptr,
+                                                                                  a.du ? a.du + c0 * NF : nullptr,
+                                                                                  a.d2u ? a.d2u + c0 * NF : nullptr));
+      }
+      continue;
+    }
+    // ---------------- residual, loss partials, seeds (a3 / a8)
+    const unsigned nb = (unsigned)((n + 255) / 256);
+    float* ybar = net->adj_a.f();
+    float* xbar = net->adj_b.f();
+    float* part = net->loss_part.f();
+    if (a.kind == PASS_INTERIOR) {
+      const hrkan_pde& pde = *a.pde;
+      const float* f = a.forcing ? a.forcing + c0 : nullptr;
+      if (pde.kind == HRKAN_BURGERS) {
+        if constexpr (NF == 2 && NS == 1)
+          HR_LAUNCH(HRKAN_K_LOSS, "k_interior_loss",
+                    k_interior_loss<2, 2, 1, true><<<nb, 256, 0, st>>>(jet[L], X0, f, ybar, part, n, pde.alpha, pde.adv, pde.visc, a.inv_n));
+        else
+          return fail(HRKAN_EINVAL, "internal: Burgers pass needs NF=2, NS=1");
+      } else {
+        if constexpr (NF == NS && NF >= 1)
+          HR_LAUNCH(HRKAN_K_LOSS, "k_interior_loss",
+                    k_interior_loss<NF, NF, NS, false><<<nb, 256, 0, st>>>(jet[L], X0, f, ybar, part, n, pde.alpha, 0.f, 0.f, a.inv_n));
+        else
+          return fail(HRKAN_EINVAL, "internal: Poisson pass needs NF=NS=D");
+      }
+      HR_LAUNCH(HRKAN_K_LOSS, "k_finish_loss",
+                k_finish_loss<<<1, 256, 0, st>>>(part, (int)nb, pde.alpha * a.inv_n, a.out_loss, a.out_flag));
+    } else {
+      HR_LAUNCH(HRKAN_K_LOSS, "k_boundary_loss", k_boundary_loss<<<nb, 256, 0, st>>>(jet[L], a.g + c0, ybar, part, n, a.inv_n));
+      HR_LAUNCH(HRKAN_K_LOSS, "k_finish_loss", k_finish_loss<<<1, 256, 0, st>>>(part, (int)nb, a.inv_n, a.out_loss, a.out_flag));
+    }
+    // ---------------- reverse (a4-a7)
+    for (int l = L - 1; l >= 0; --l) {
+      const int I = net->widths[l], O = net->widths[l + 1];
+      const float* in = (l == 0) ? X0 : jet[l];
+      float* dW = a.grad + net->w_off[l];
+      float* db = a.grad + net->b_off[l];
+      bool done = false;
+      if (l > 0 && l < L - 1) HR_TRY(tc_wgrad_layer<NF, NS, M>(net, l, in, ybar, dW, db, n, st, &done));
+      if (!done) {
+        const dim3 blk(WG_J, WG_I);
+        const int gx = (O + WG_J - 1) / WG_J, gy = (I + WG_I - 1) / WG_I;
+        int nz = (int)std::max<int64_t>(1, (4 * net->num_sms + gx * gy - 1) / (gx * gy));
+        nz = (int)std::min<int64_t>(nz, std::max<int64_t>(1, n / 64));
+        nz = std::min(nz, NZ_MAX);
+        const dim3 grid(gx, gy, nz);
+        const size_t smem = sizeof(float) * WG_I * net->B * WG_J;
+        const int cls = (l == 0) ? HRKAN_K_WGRAD_FIRST : (l == L - 1 ? HRKAN_K_WGRAD_LAST : HRKAN_K_WGRAD_HIDDEN);
+        if (l == 0) {
+          auto kfn = k_wgrad_simt<NF, NS, M, true>;
+          if (smem > 48 * 1024) HR_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+          HR_LAUNCH(cls, "k_wgrad_simt", kfn<<<grid, blk, smem, st>>>(in, ybar, net->w_part.f(), net->b_part.f(), n, I, O, bc));
+        } else {
+          auto kfn = k_wgrad_simt<NF, NS, M, false>;
+          if (smem > 48 * 1024) HR_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+          HR_LAUNCH(cls, "k_wgrad_simt", kfn<<<grid, blk, smem, st>>>(in, ybar, net->w_part.f(), net->b_part.f(), n, I, O, bc));
+        }
+        const int64_t nW = (int64_t)O * I * net->B;
+        HR_LAUNCH(HRKAN_K_REDUCE, "k_reduce_parts",
+                  k_reduce_parts<<<(unsigned)((nW + O + 255) / 256), 256, 0, st>>>(net->w_part.f(), net->b_part.f(), nz, nW, O, dW, db));
+      }
+      if (l > 0) {
+        bool ddone = false;
+        if (l < L - 1) HR_TRY(tc_dgrad_layer<NF, NS, M>(net, l, in, ybar, xbar, n, st, &ddone));
+        if (!ddone) {
+          const int64_t tot = n * I;
+          HR_LAUNCH(l == L - 1 ? HRKAN_K_DGRAD_LAST : HRKAN_K_DGRAD_HIDDEN, "k_dgrad_simt",
+                    k_dgrad_simt<NF, NS, M><<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(in, net->params + net->w_off[l], ybar, xbar, n, I, O, bc));
+        }
+        std::swap(ybar, xbar);
+      }
+    }
+  }
+  return HRKAN_OK;
+}
+
+template <class F>
+hrkan_status with_channels(int nf, int ns, F&& f) {
+  if (nf == 0 && ns == 0) return f(IC<0>{}, IC<0>{});
+  if (nf == 1 && ns == 1) return f(IC<1>{}, IC<1>{});
+  if (nf == 2 && ns == 1) return f(IC<2>{}, IC<1>{});
+  if (nf == 2 && ns == 2) return f(IC<2>{}, IC<2>{});
+  if (nf == 3 && ns == 3) return f(IC<3>{}, IC<3>{});
+  return fail(HRKAN_EINVAL, "internal: unsupported channel set");
+}
+
+hrkan_status dispatch_pass(hrkan_net* net, int nf, int ns, const PassArgs& a, cudaStream_t st) {
+  return with_channels(nf, ns, [&](auto NFc, auto NSc) {
+    return with_m(net->m, [&](auto Mc) {
+      return run_pass<decltype(NFc)::value, decltype(NSc)::value, decltype(Mc)::value>(net, a, st);
+    });
+  });
+}
+
+}  // namespace
+
+// =============================================================================================
+// C ABI
+// =============================================================================================
+extern "C" {
+
+const char* hrkan_last_error(void) { return g_err.c_str(); }
+
+hrkan_status hrkan_create(const int32_t* widths, int32_t n_widths, int32_t G, int32_t k, int32_t m, float grid_lo,
+                          float grid_hi, uint64_t seed, int32_t device, hrkan_net_t* out) {
+  g_err.clear();
+  if (!out) return fail(HRKAN_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (!widths || n_widths < 2) return fail(HRKAN_EINVAL, "need at least 2 widths");
+  for (int i = 0; i < n_widths; ++i)
+    if (widths[i] < 1) return fail(HRKAN_EINVAL, "widths must be >= 1");
+  if (widths[0] < 1 || widths[0] > 3) return fail(HRKAN_EINVAL, "widths[0] (input dimension D) must be 1, 2 or 3");
+  if (widths[n_widths - 1] != 1) return fail(HRKAN_EINVAL, "the last width must be 1 (scalar PDE solution)");
+  if (G < 1 || k < 1) return fail(HRKAN_EINVAL, "G and k must be >= 1");
+  if (k + 1 > KMAX) return fail(HRKAN_EUNSUPPORTED, "k > 7 is not supported");
+  if (G + k > 200) return fail(HRKAN_EUNSUPPORTED, "G + k > 200 is not supported");
+  if (m < 2 || m > 8) return fail(HRKAN_EINVAL, "m must be in [2, 8] (second derivatives need m >= 2)");
+  if (!std::isfinite(grid_lo) || !std::isfinite(grid_hi) || !(grid_lo < grid_hi))
+    return fail(HRKAN_EINVAL, "grid_lo < grid_hi (finite) required");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
+    cudaGetLastError();
+    return fail(HRKAN_EINVAL, "invalid CUDA device index");
+  }
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return fail(HRKAN_ECUDA, "cudaGetDeviceProperties failed");
+  if (prop.major != 10 || prop.minor != 0)
+    return fail(HRKAN_EUNSUPPORTED, "libhrkan is built for sm_100a (B200) only; device is sm_" +
+                                        std::to_string(prop.major) + std::to_string(prop.minor));
+  DeviceGuard dg(device);
+  hrkan_net* net = new hrkan_net();
+  net->device = device;
+  net->num_sms = prop.multiProcessorCount;
+  net->widths.assign(widths, widths + n_widths);
+  net->L = n_widths - 1;
+  net->D = widths[0];
+  net->G = G;
+  net->k = k;
+  net->m = m;
+  net->B = G + k;
+  net->lo = grid_lo;
+  net->hi = grid_hi;
+  const double h = ((double)grid_hi - grid_lo) / G;
+  net->bc.lo = grid_lo;
+  net->bc.h = (float)h;
+  net->bc.inv_h = (float)(1.0 / h);
+  net->bc.sc = (float)(2.0 / ((k + 1) * h));
+  net->bc.mid0 = (float)(grid_lo + 0.5 * (1 - k) * h);
+  net->bc.k = k;
+  net->bc.B = G + k;
+  int64_t off = 0;
+  for (int l = 0; l < net->L; ++l) {
+    const int64_t nW = (int64_t)widths[l + 1] * widths[l] * net->B;
+    net->w_off.push_back(off);
+    off += nW;
+    net->b_off.push_back(off);
+    off += widths[l + 1];
+    net->max_layer_w = std::max(net->max_layer_w, nW);
+    net->max_width = std::max(net->max_width, widths[l + 1]);
+  }
+  net->n_params = off;
+  auto cleanup = [&](hrkan_status s) {
+    hrkan_free(net);
+    return s;
+  };
+  if (cudaMalloc(&net->params, sizeof(float) * off) != cudaSuccess ||
+      cudaMalloc(&net->adam_m, sizeof(float) * off) != cudaSuccess ||
+      cudaMalloc(&net->adam_v, sizeof(float) * off) != cudaSuccess) {
+    cudaGetLastError();
+    return cleanup(fail(HRKAN_ENOMEM, "parameter allocation failed"));
+  }
+  net->wt.assign(net->L, nullptr);
+  for (int l = 0; l < net->L; ++l) {
+    if (cudaMalloc(&net->wt[l], sizeof(float) * (size_t)widths[l + 1] * widths[l] * net->B) != cudaSuccess) {
+      cudaGetLastError();
+      return cleanup(fail(HRKAN_ENOMEM, "weight copy allocation failed"));
+    }
+  }
+  hrkan_status s = hrkan_init_params(net, seed, nullptr);
+  if (s != HRKAN_OK) return cleanup(s);
+  if (cudaDeviceSynchronize() != cudaSuccess) return cleanup(fail(HRKAN_ECUDA, "init failed"));
+  *out = net;
+  return HRKAN_OK;
+}
+
+int64_t hrkan_num_params(hrkan_net_t net) { return net ? net->n_params : -1; }
+
+int64_t hrkan_launch_count(hrkan_net_t net) { return net ? net->launches : -1; }
+
+hrkan_status hrkan_set_chunk_points(hrkan_net_t net, int64_t chunk) {
+  if (!net) return fail(HRKAN_EINVAL, "net is NULL");
+  if (chunk < 0) return fail(HRKAN_EINVAL, "chunk must be >= 0");
+  net->chunk = chunk == 0 ? 0 : std::max<int64_t>(1, chunk);
+  return HRKAN_OK;
+}
+
+hrkan_status hrkan_set_engine(hrkan_net_t net, int32_t mode) {
+  if (!net) return fail(HRKAN_EINVAL, "net is NULL");
+  if (mode < 0 || mode > 2) return fail(HRKAN_EINVAL, "engine mode must be 0, 1 or 2");
+  net->engine = mode;
+  return HRKAN_OK;
+}
+
+hrkan_status hrkan_init_params(hrkan_net_t net, uint64_t seed, void* stream) {
+  if (!net) return fail(HRKAN_EINVAL, "net is NULL");
+  DeviceGuard dg(net->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  for (int l = 0; l < net->L; ++l) {
+    const int I = net->widths[l], O = net->widths[l + 1];
+    const int64_t nW = (int64_t)O * I * net->B;
+    const float stdv = (float)(1.0 / std::sqrt((double)I * net->B));
+    const int64_t n = std::max<int64_t>(nW, O);
+    k_init_layer<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(net->params + net->w_off[l], net->params + net->b_off[l], nW, O,
+                                                              stdv, seed, (uint32_t)l);
+    HR_TRY(check_launch(net, "k_init_layer"));
+  }
+  HR_CUDA(cudaMemsetAsync(net->adam_m, 0, sizeof(float) * net->n_params, st));
+  HR_CUDA(cudaMemsetAsync(net->adam_v, 0, sizeof(float) * net->n_params, st));
+  net->adam_t = 0;
+  net->derived_dirty = true;
+  return HRKAN_OK;
+}
+
+hrkan_status hrkan_get_params(hrkan_net_t net, float* dst, void* stream) {
+  if (!net || !dst) return fail(HRKAN_EINVAL, "NULL argument");
+  DeviceGuard dg(net->device);
+  HR_CUDA(cudaMemcpyAsync(dst, net->params, sizeof(float) * net->n_params, cudaMemcpyDefault, (cudaStream_t)stream));
+  return HRKAN_OK;
+}
+
+hrkan_status hrkan_set_params(hrkan_net_t net, const float* src, void* stream) {
+  if (!net || !src) return fail(HRKAN_EINVAL, "NULL argument");
+  DeviceGuard dg(net->device);
+  HR_CUDA(cudaMemcpyAsync(net->params, src, sizeof(float) * net->n_params, cudaMemcpyDefault, (cudaStream_t)stream));
+  net->derived_dirty = true;
+  return HRKAN_OK;
+}
+
+hrkan_status hrkan_forward_jet(hrkan_net_t net, const float* pts, int64_t P, float* u, float* du, float* d2u,
+                               void* stream) {
+  if (!net) return fail(HRKAN_EINVAL, "net is NULL");
+  if (P < 0) return fail(HRKAN_EINVAL, "P must be >= 0");
+  if (P == 0) return HRKAN_OK;
+  if (!pts) return fail(HRKAN_EINVAL, "pts is NULL");
+  g_err.clear();
+  DeviceGuard dg(net->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int D = net->D;
+  const float* dpts;
+  HR_TRY(stage_in(pts, P * D, net->st_pts, st, &dpts));
+  float* du_dev = du;
+  float* u_dev = u;
+  float* d2u_dev = d2u;
+  const bool hu = u && !is_device_ptr(u), hdu = du && !is_device_ptr(du), hd2u = d2u && !is_device_ptr(d2u);
+  if (hu) { HR_CUDA(net->st_u.ensure(sizeof(float) * P)); u_dev = net->st_u.f(); }
+  if (hdu) { HR_CUDA(net->st_du.ensure(sizeof(float) * P * D)); du_dev = net->st_du.f(); }
+  if (hd2u) { HR_CUDA(net->st_d2u.ensure(sizeof(float) * P * D)); d2u_dev = net->st_d2u.f(); }
+  HR_TRY(refresh_derived(net, st));
+  PassArgs a{};
+  a.kind = PASS_JET;
+  a.pts = dpts;
+  a.P = P;
+  a.u = u_dev;
+  a.du = du_dev;
+  a.d2u = d2u_dev;
+  HR_TRY(dispatch_pass(net, D, D, a, st));
+  if (hu) HR_CUDA(cudaMemcpyAsync(u, u_dev, sizeof(float) * P, cudaMemcpyDeviceToHost, st));
+  if (hdu) HR_CUDA(cudaMemcpyAsync(du, du_dev, sizeof(float) * P * D, cudaMemcpyDeviceToHost, st));
+  if (hd2u) HR_CUDA(cudaMemcpyAsync(d2u, d2u_dev, sizeof(float) * P * D, cudaMemcpyDeviceToHost, st));
+  return HRKAN_OK;
+}
+
+hrkan_status hrkan_pinn_loss_grad(hrkan_net_t net, const hrkan_pde* pde, const float* interior, const float* forcing,
+                                  int64_t Ni, const float* boundary, const float* g_boundary, int64_t Nb,
+                                  const float* initial, const float* g_initial, int64_t N0, int64_t Ni_global,
+                                  int64_t Nbi_global, float* out, void* stream) {
+  if (!net) return fail(HRKAN_EINVAL, "net is NULL");
+  if (!pde) return fail(HRKAN_EINVAL, "pde is NULL");
+  if (!out) return fail(HRKAN_EINVAL, "out is NULL");
+  if (Ni < 0 || Nb < 0 || N0 < 0) return fail(HRKAN_EINVAL, "negative point count");
+  if ((Ni > 0 && !interior) || (Nb > 0 && (!boundary || !g_boundary)) || (N0 > 0 && (!initial || !g_initial)))
+    return fail(HRKAN_EINVAL, "NULL point/target buffer with a non-zero count");
+  if (Ni_global < Ni || Nbi_global < Nb + N0) return fail(HRKAN_EINVAL, "global normalisers smaller than local counts");
+  if (pde->kind != HRKAN_POISSON && pde->kind != HRKAN_BURGERS) return fail(HRKAN_EINVAL, "unknown pde kind");
+  if (pde->kind == HRKAN_BURGERS && net->D != 2) return fail(HRKAN_EINVAL, "Burgers needs D = 2 (x, t)");
+  if (!std::isfinite(pde->alpha)) return fail(HRKAN_EINVAL, "alpha must be finite");
+  g_err.clear();
+  DeviceGuard dg(net->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int D = net->D;
+  const int64_t np = net->n_params;
+  const float *d_int, *d_f = nullptr, *d_bnd, *d_gb, *d_ini, *d_gi;
+  HR_TRY(stage_in(interior, Ni * D, net->st_int, st, &d_int));
+  if (forcing && pde->kind == HRKAN_POISSON) HR_TRY(stage_in(forcing, Ni, net->st_f, st, &d_f));
+  HR_TRY(stage_in(boundary, Nb * D, net->st_bnd, st, &d_bnd));
+  HR_TRY(stage_in(g_boundary, Nb, net->st_gb, st, &d_gb));
+  HR_TRY(stage_in(initial, N0 * D, net->st_ini, st, &d_ini));
+  HR_TRY(stage_in(g_initial, N0, net->st_gi, st, &d_gi));
+  float* dout = out;
+  const bool host_out = !is_device_ptr(out);
+  if (host_out) {
+    HR_CUDA(net->st_out.ensure(sizeof(float) * (np + 4)));
+    dout = net->st_out.f();
+  }
+  HR_CUDA(cudaMemsetAsync(dout, 0, sizeof(float) * (np + 4), st));
+  HR_TRY(refresh_derived(net, st));
+  PassArgs a{};
+  a.grad = dout;
+  a.pde = pde;
+  a.out_flag = dout + np + 2;
+  if (Ni > 0) {
+    a.kind = PASS_INTERIOR;
+    a.pts = d_int;
+    a.P = Ni;
+    a.forcing = d_f;
+    a.out_loss = dout + np;
+    a.inv_n = (float)(1.0 / (double)Ni_global);
+    const int nf = D, ns = (pde->kind == HRKAN_BURGERS) ? 1 : D;
+    HR_TRY(dispatch_pass(net, nf, ns, a, st));
+  }
+  a.kind = PASS_BOUNDARY;
+  a.out_loss = dout + np + 1;
+  a.inv_n = Nbi_global > 0 ? (float)(1.0 / (double)Nbi_global) : 0.f;
+  a.forcing = nullptr;
+  if (Nb > 0) {
+    a.pts = d_bnd;
+    a.P = Nb;
+    a.g = d_gb;
+    HR_TRY(dispatch_pass(net, 0, 0, a, st));
+  }
+  if (N0 > 0) {
+    a.pts = d_ini;
+    a.P = N0;
+    a.g = d_gi;
+    HR_TRY(dispatch_pass(net, 0, 0, a, st));
+  }
+  if (host_out) HR_CUDA(cudaMemcpyAsync(out, dout, sizeof(float) * (np + 4), cudaMemcpyDeviceToHost, st));
+  return HRKAN_OK;
+}
+
+hrkan_status hrkan_adam_step(hrkan_net_t net, const float* grad, float lr, float beta1, float beta2, float eps,
+                             void* stream) {
+  if (!net || !grad) return fail(HRKAN_EINVAL, "NULL argument");
+  if (!std::isfinite(lr) || !std::isfinite(eps) || !(beta1 >= 0.f && beta1 < 1.f) || !(beta2 >= 0.f && beta2 < 1.f))
+    return fail(HRKAN_EINVAL, "invalid Adam hyper-parameters");
+  DeviceGuard dg(net->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  const float* dg_ptr;
+  HR_TRY(stage_in(grad, net->n_params, net->st_out, st, &dg_ptr));
+  net->adam_t += 1;
+  const double bc1 = 1.0 - std::pow((double)beta1, (double)net->adam_t);
+  const double bc2 = 1.0 - std::pow((double)beta2, (double)net->adam_t);
+  const int64_t n = net->n_params;
+  HR_LAUNCH(HRKAN_K_ADAM, "k_adam",
+            k_adam<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(net->params, net->adam_m, net->adam_v, dg_ptr, n, lr, beta1,
+                                                                beta2, eps, (float)(1.0 / bc1), (float)(1.0 / bc2)));
+  net->derived_dirty = true;
+  return HRKAN_OK;
+}
+
+hrkan_status hrkan_profile_enable(hrkan_net_t net, int32_t enable) {
+  if (!net) return fail(HRKAN_EINVAL, "net is NULL");
+  net->prof_on = enable != 0;
+  return HRKAN_OK;
+}
+
+hrkan_status hrkan_profile_read(hrkan_net_t net, double* ms, int64_t* n) {
+  if (!net) return fail(HRKAN_EINVAL, "net is NULL");
+  DeviceGuard dg(net->device);
+  double acc[HRKAN_K_NUM_CLASSES] = {0};
+  int64_t cnt[HRKAN_K_NUM_CLASSES] = {0};
+  for (size_t i = 0; i < net->prof_used; ++i) {
+    const auto& ev = net->prof_pool[i];
+    HR_CUDA(cudaEventSynchronize(ev.b));
+    float t = 0.f;
+    HR_CUDA(cudaEventElapsedTime(&t, ev.a, ev.b));
+    acc[ev.cls] += t;
+    cnt[ev.cls] += 1;
+  }
+  net->prof_used = 0;
+  for (int c = 0; c < HRKAN_K_NUM_CLASSES; ++c) {
+    if (ms) ms[c] = acc[c];
+    if (n) n[c] = cnt[c];
+  }
+  return HRKAN_OK;
+}
+
+void hrkan_free(hrkan_net_t net) {
+  if (!net) return;
+  DeviceGuard dg(net->device);
+  cudaDeviceSynchronize();
+  for (auto& ev : net->prof_pool) {
+    cudaEventDestroy(ev.a);
+    cudaEventDestroy(ev.b);
+  }
+  cudaFree(net->params);
+  cudaFree(net->adam_m);
+  cudaFree(net->adam_v);
+  for (float* p : net->wt) cudaFree(p);
+  DevBuf* bufs[] = {&net->jets, &net->adj_a, &net->adj_b, &net->loss_part, &net->w_part, &net->b_part,
+                    &net->st_int, &net->st_f, &net->st_bnd, &net->st_gb, &net->st_ini, &net->st_gi,
+                    &net->st_out, &net->st_pts, &net->st_u, &net->st_du, &net->st_d2u, &net->tc_ws};
+  for (DevBuf* b : bufs) b->release();
+  delete net;
+}
+
+}  // extern "C"

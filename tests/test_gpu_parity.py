@@ -1,0 +1,284 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the float64 oracle on identical seeded inputs.
+
+Tolerances (BASELINE.json north_star, relative L2 over each tensor):
+  u 1e-4, du 5e-4, d2u 2e-3, loss 2e-3, every dL/dW_l, dL/db_l and the flat gradient 2e-3.
+Parity sets (SURVEY.md §8(c) "Parity protocol"): full sets for C1/C2, strided subsets for C3-C5,
+with a small chunk size so that several chunks and a ragged tail are exercised."""
+import math
+
+import numpy as np
+import pytest
+
+import hrkan_inputs as HI
+from oracle import hrkan_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"u": 1e-4, "du": 5e-4, "d2u": 2e-3, "loss": 2e-3, "grad": 2e-3}
+SUBSETS = {"C1": (1, 1), "C2": (1, 1), "C3": (64, 4), "C4": (1024, 64), "C5": (8192, 256)}
+
+
+def rel_l2(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
+
+
+@pytest.fixture(scope="module")
+def torch_mod():
+    import torch
+    assert torch.cuda.is_available()
+    return torch
+
+
+def _pde(w):
+    return {"kind": w.pde, "alpha": w.alpha, "adv": w.adv, "visc": w.visc}
+
+
+def _make(w, seed=7, bias_std=0.1, engine=None, chunk=None):
+    from paper_2409_14248_b200 import HRKANNet
+    net = HRKANNet(w.widths, w.G, w.k, w.m)
+    params = HI.random_params(w.widths, w.G, w.k, seed=seed, bias_std=bias_std)
+    net.set_params(HI.flatten_params(params))
+    if engine is not None:
+        net.set_engine(engine)
+    if chunk is not None:
+        net.set_chunk_points(chunk)
+    return net, params
+
+
+def _oracle_net(w):
+    return O.Net(w.widths, w.G, w.k, w.m, w.lo, w.hi)
+
+
+def _workloads():
+    out = [HI.WORKLOADS["C1"], HI.WORKLOADS["C2"], HI.WORKLOADS["C3"]]
+    out += [HI.WORKLOADS["C4"].with_m(m) for m in (2, 3, 4)]
+    out += [HI.WORKLOADS["C5"]]
+    return out
+
+
+def _points(w):
+    ps = HI.make_points(w)
+    si, sb = SUBSETS[w.key.split("_")[0]]
+    return ps.subset(si, sb)
+
+
+@pytest.mark.parametrize("w", _workloads(), ids=lambda w: w.key)
+def test_forward_jet_parity(torch_mod, w):
+    torch = torch_mod
+    net, params = _make(w, chunk=1000)          # several chunks + ragged tail
+    ps = _points(w)
+    pts = ps.interior[:3000]
+    u, du, d2u = net.forward_jet(torch.from_numpy(pts).cuda())
+    torch.cuda.synchronize()
+    ou, odu, od2u = O.forward_jet(_oracle_net(w), params, pts)
+    assert rel_l2(u.cpu().numpy(), ou) < TOL["u"]
+    assert rel_l2(du.cpu().numpy(), odu) < TOL["du"]
+    assert rel_l2(d2u.cpu().numpy(), od2u) < TOL["d2u"]
+
+
+def _loss_grad_gpu(torch, net, w, ps, **kw):
+    from paper_2409_14248_b200 import pde_struct
+    cu = lambda a: None if a is None else torch.from_numpy(a).cuda()
+    out = net.pinn_loss_grad(pde_struct(w.pde, w.alpha, w.adv, w.visc), cu(ps.interior), cu(ps.boundary),
+                             cu(ps.g_boundary), cu(ps.initial), cu(ps.g_initial), **kw)
+    torch.cuda.synchronize()
+    return out.cpu().numpy()
+
+
+def _loss_grad_oracle(w, params, ps, **kw):
+    bi = ps.boundary if ps.initial is None else np.concatenate([ps.boundary, ps.initial])
+    gbi = ps.g_boundary if ps.initial is None else np.concatenate([ps.g_boundary, ps.g_initial])
+    lp, lb, g = O.loss_grad(_oracle_net(w), params, _pde(w), ps.interior, bi, gbi, **kw)
+    return lp, lb, g
+
+
+def _check_loss_grad(out, w, lp, lb, g):
+    np_ = w.num_params()
+    assert out[np_ + 2] == 0.0                      # no non-finite values
+    assert abs(out[np_] - lp) <= TOL["loss"] * abs(lp) + 1e-12
+    assert abs(out[np_ + 1] - lb) <= TOL["loss"] * abs(lb) + 1e-12
+    flat = O.flat_grad(g)
+    assert rel_l2(out[:np_], flat) < TOL["grad"]
+    gl = HI.unflatten_params(out[:np_].copy(), w.widths, w.B)
+    for l, ((gW, gb), (oW, ob)) in enumerate(zip(gl, g)):
+        assert rel_l2(gW, oW) < TOL["grad"], f"dW layer {l}"
+        assert rel_l2(gb, ob) < TOL["grad"], f"db layer {l}"
+
+
+@pytest.mark.parametrize("w", _workloads(), ids=lambda w: w.key)
+def test_loss_grad_parity(torch_mod, w):
+    torch = torch_mod
+    ps = _points(w)
+    net, params = _make(w, chunk=4000 if w.n_int > 20000 else None)
+    out = _loss_grad_gpu(torch, net, w, ps)
+    lp, lb, g = _loss_grad_oracle(w, params, ps)
+    _check_loss_grad(out, w, lp, lb, g)
+
+
+def test_loss_grad_parity_simt_engine_c3(torch_mod):
+    """The SIMT engine alone (the reference engine for every tensor-core kernel)."""
+    torch = torch_mod
+    w = HI.WORKLOADS["C3"]
+    ps = HI.make_points(w).subset(256, 16)
+    net, params = _make(w, engine=1)
+    out = _loss_grad_gpu(torch, net, w, ps)
+    _check_loss_grad(out, w, *_loss_grad_oracle(w, params, ps))
+
+
+def test_polynomial_chain_net_exact_gpu(torch_mod):
+    """P3: a chain through neuron 0 of a [3,256,256,1] net, all other weights 0 (mostly-zero
+    tiles): the GPU reproduces the exact laplacian from rational arithmetic."""
+    import sympy as sp
+    from tests.test_oracle_jet_loss_grad import _p2_setup
+    from paper_2409_14248_b200 import HRKANNet
+    torch = torch_mod
+    widths = (3, 256, 256, 1)
+    syms, u, params, (G, k, lo, hi) = _p2_setup(4, widths, 3)
+    net = HRKANNet(list(widths), G, k, 4, lo, hi)
+    net.set_params(HI.flatten_params([(W.astype(np.float32), b.astype(np.float32)) for W, b in params]))
+    rng = np.random.default_rng(3)
+    pts = [[sp.Rational(int(rng.integers(-59, 99)), 100) for _ in range(3)] for _ in range(4)]
+    P = np.array([[float(a) for a in p] for p in pts], np.float32)
+    gu, gdu, gd2u = [t.cpu().numpy() for t in net.forward_jet(torch.from_numpy(P).cuda())]
+    for q, p in enumerate(pts):
+        sub = dict(zip(syms, p))
+        ref_u = float(u.subs(sub))
+        ref_lap = float(sum(sp.diff(u, z, 2) for z in syms).subs(sub))
+        assert gu[q] == pytest.approx(ref_u, rel=1e-4, abs=1e-5)
+        assert gd2u[q].sum() == pytest.approx(ref_lap, rel=2e-3, abs=1e-3)
+
+
+def test_host_buffers_match_device_buffers(torch_mod):
+    """The same call with HOST (numpy) buffers is staged by the library and gives identical bits."""
+    torch = torch_mod
+    from paper_2409_14248_b200 import pde_struct
+    w = HI.WORKLOADS["C2"]
+    ps = HI.make_points(w)
+    net, _ = _make(w)
+    dev = _loss_grad_gpu(torch, net, w, ps)
+    host_out = np.zeros(w.num_params() + 4, np.float32)
+    net.pinn_loss_grad(pde_struct(w.pde, w.alpha, w.adv, w.visc), ps.interior, ps.boundary, ps.g_boundary,
+                       ps.initial, ps.g_initial, out=host_out)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(host_out, dev)
+
+
+def test_determinism_and_chunk_invariance(torch_mod):
+    torch = torch_mod
+    w = HI.WORKLOADS["C3"]
+    ps = HI.make_points(w).subset(128, 4)
+    net, _ = _make(w)
+    a = _loss_grad_gpu(torch, net, w, ps)
+    b = _loss_grad_gpu(torch, net, w, ps)
+    np.testing.assert_array_equal(a, b)               # run-to-run bitwise reproducible
+    net.set_chunk_points(777)                          # ragged chunks: same result up to fp32 order
+    c = _loss_grad_gpu(torch, net, w, ps)
+    assert rel_l2(c, a) < 1e-5
+
+
+def test_fake_collective_shards_sum(torch_mod):
+    """Shards evaluated one after another with global normalisers sum to the unsharded call."""
+    torch = torch_mod
+    w = HI.WORKLOADS["C2"]
+    ps = HI.make_points(w)
+    net, _ = _make(w)
+    full = _loss_grad_gpu(torch, net, w, ps)
+    acc = np.zeros_like(full, dtype=np.float64)
+    for r in range(4):
+        sh = ps.shard(r, 4)
+        acc += _loss_grad_gpu(torch, net, w, sh, n_int_global=len(ps.interior), n_bi_global=ps.n_bi)
+    assert rel_l2(acc, full) < 1e-5
+
+
+def test_edge_cases(torch_mod):
+    torch = torch_mod
+    from paper_2409_14248_b200 import pde_struct, HrkanError
+    w = HI.WORKLOADS["C1"]
+    net, params = _make(w)
+    # P = 0 forward is a no-op
+    u, du, d2u = net.forward_jet(torch.zeros(0, 2, device="cuda"))
+    assert u.numel() == 0
+    # interior only (no boundary points) and boundary only
+    ps = HI.make_points(w)
+    e = HI.PointSet(ps.interior[:0], ps.boundary, ps.g_boundary)
+    out = _loss_grad_gpu(torch, net, w, e)
+    lp, lb, g = _loss_grad_oracle(w, params, e)
+    assert out[w.num_params()] == 0.0
+    _check_loss_grad(out, w, lp, lb, g)
+    e2 = HI.PointSet(ps.interior[:37], ps.boundary[:0], ps.g_boundary[:0])
+    out = _loss_grad_gpu(torch, net, w, e2)
+    _check_loss_grad(out, w, *_loss_grad_oracle(w, params, e2))
+    # non-finite inputs are flagged, not hidden
+    bad = HI.PointSet(ps.interior[:10].copy(), ps.boundary[:4], ps.g_boundary[:4].copy())
+    bad.interior[3, 0] = np.nan
+    bad.g_boundary[1] = np.inf
+    out = _loss_grad_gpu(torch, net, w, bad)
+    assert out[w.num_params() + 2] == 2.0
+    # invalid arguments raise
+    with pytest.raises(HrkanError):
+        net.pinn_loss_grad(pde_struct("burgers"), torch.zeros(4, 2, device="cuda"), torch.zeros(0, 2, device="cuda"),
+                           torch.zeros(0, device="cuda"), n_int_global=2)
+
+
+def test_points_outside_grid_and_m2_knots(torch_mod):
+    """Hidden/input values beyond [lo-kh, hi+kh] give all-zero features (no clamping)."""
+    torch = torch_mod
+    w = HI.WORKLOADS["C2"]
+    net, params = _make(w, seed=3)
+    pts = np.random.default_rng(0).uniform(-3, 3, (500, 2)).astype(np.float32)
+    u, du, d2u = [t.cpu().numpy() for t in net.forward_jet(torch.from_numpy(pts).cuda())]
+    ou, odu, od2u = O.forward_jet(_oracle_net(w), params, pts)
+    assert rel_l2(u, ou) < TOL["u"] and rel_l2(du, odu) < TOL["du"] and rel_l2(d2u, od2u) < TOL["d2u"]
+
+
+def test_adam_parity(torch_mod):
+    torch = torch_mod
+    w = HI.WORKLOADS["C2"]
+    net, params = _make(w)
+    theta = HI.flatten_params(params).astype(np.float64)
+    m = np.zeros_like(theta)
+    v = np.zeros_like(theta)
+    rng = np.random.default_rng(0)
+    for t in range(1, 4):
+        g = rng.standard_normal(len(theta)).astype(np.float32)
+        net.adam_step(torch.from_numpy(g).cuda(), lr=1e-2)
+        theta, m, v = O.adam_step(theta, g.astype(np.float64), m, v, t, lr=1e-2)
+    got = net.get_params().cpu().numpy()
+    np.testing.assert_allclose(got, theta, rtol=1e-5, atol=1e-6)
+
+
+def test_init_distribution(torch_mod):
+    """W ~ N(0, 1/(I (G+k))) per layer (variance reading), b = 0, deterministic per seed."""
+    from paper_2409_14248_b200 import HRKANNet
+    w = HI.WORKLOADS["C5"]
+    a = HRKANNet(w.widths, w.G, w.k, w.m, seed=11)
+    b = HRKANNet(w.widths, w.G, w.k, w.m, seed=11)
+    c = HRKANNet(w.widths, w.G, w.k, w.m, seed=12)
+    pa, pb, pc = [n.get_params().cpu().numpy() for n in (a, b, c)]
+    np.testing.assert_array_equal(pa, pb)
+    assert not np.array_equal(pa, pc)
+    for l, (W, bb) in enumerate(HI.unflatten_params(pa, w.widths, w.B)):
+        var = 1.0 / (w.widths[l] * w.B)
+        assert np.all(bb == 0)
+        n = W.size
+        assert abs(W.mean()) < 5 * math.sqrt(var / n)
+        assert abs(W.var() / var - 1) < 5 * math.sqrt(2.0 / n) + 1e-3
+
+
+def test_full_size_forward_sampled(torch_mod):
+    """Full BASELINE size (C3, 2^20 interior points, default chunking = bench launch config):
+    sampled outputs checked one by one against the oracle."""
+    torch = torch_mod
+    w = HI.WORKLOADS["C3"]
+    ps = HI.make_points(w)
+    net, params = _make(w)
+    u, du, d2u = [t.cpu().numpy() for t in net.forward_jet(torch.from_numpy(ps.interior).cuda())]
+    idx = np.random.default_rng(0).choice(len(ps.interior), 256, replace=False)
+    ou, odu, od2u = O.forward_jet(_oracle_net(w), params, ps.interior[idx])
+    assert rel_l2(u[idx], ou) < TOL["u"]
+    assert rel_l2(du[idx], odu) < TOL["du"]
+    assert rel_l2(d2u[idx], od2u) < TOL["d2u"]
+    assert np.all(np.isfinite(u)) and np.all(np.isfinite(d2u))
