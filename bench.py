@@ -171,8 +171,11 @@ def time_oracle(w: HI.Workload, ps: HI.PointSet, target_s: float):
 
     n = 16
     dt, npts = run(oracle_sample(w, ps, n))
-    while dt < target_s / 8 and n < len(ps.interior):
-        n = min(len(ps.interior), int(n * max(2.0, min(16.0, (target_s / 4) / max(dt, 1e-3)))))
+    while dt < target_s / 10 and n < len(ps.interior):     # grow the probe geometrically
+        n = min(len(ps.interior), n * 4)
+        dt, npts = run(oracle_sample(w, ps, n))
+    if dt < 0.5 * target_s and n < len(ps.interior):         # final sample sized for ~target_s
+        n = min(len(ps.interior), int(n * target_s / max(dt, 1e-3)))
         dt, npts = run(oracle_sample(w, ps, n))
     sample = oracle_sample(w, ps, n)
     desc = (f"{w.key} strided sample: {len(sample.interior)} interior + {sample.n_bi} boundary/initial points "

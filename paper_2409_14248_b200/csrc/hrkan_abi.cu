@@ -89,6 +89,14 @@ struct DevBuf {
   float* f() const { return static_cast<float*>(p); }
 };
 
+// Per-layer state of the tensor-core engine (tc_kernels.cuh).
+struct TcLayerState {
+  float* w_fwd = nullptr;   // pre-tiled, pre-split W for the forward kernel
+  float* w_dgr = nullptr;   // pre-tiled, pre-split W^T for the dgrad kernel
+  int nkb = 0;              // forward K-blocks
+  int ntile_dgr = 0;        // dgrad M-tiles
+};
+
 }  // namespace
 
 struct hrkan_net {
@@ -114,15 +122,14 @@ struct hrkan_net {
   // workspace
   DevBuf jets, adj_a, adj_b, loss_part, w_part, b_part;
   DevBuf st_int, st_f, st_bnd, st_gb, st_ini, st_gi, st_out, st_pts, st_u, st_du, st_d2u;
-  DevBuf tc_ws;                         // tensor-core path scratch (split weights, hi/lo jets)
+  DevBuf tc_ws;                         // tensor-core path scratch
+  std::vector<TcLayerState> tc_layers;
   // device-time profiling (hrkan_profile_enable / hrkan_profile_read)
   struct ProfEv { cudaEvent_t a, b; int cls; };
   bool prof_on = false;
   std::vector<ProfEv> prof_pool;
   size_t prof_used = 0;
 };
-
-#include "tc_kernels.cuh"   // tensor-core (tcgen05) hidden-layer engine; needs hrkan_net
 
 namespace {
 
@@ -158,6 +165,12 @@ hrkan_status check_launch(hrkan_net* net, const char* what, int cls = HRKAN_K_OT
     __VA_ARGS__;                                                    \
     HR_TRY(check_launch(net, NAME, CLS, st, pi_));                  \
   } while (0)
+
+}  // namespace
+
+#include "tc_kernels.cuh"   // tensor-core (tcgen05) hidden-layer engine; needs hrkan_net + helpers
+
+namespace {
 
 int64_t auto_chunk(const hrkan_net* net) {
   if (net->chunk > 0) return net->chunk;
@@ -684,6 +697,7 @@ void hrkan_free(hrkan_net_t net) {
                     &net->st_int, &net->st_f, &net->st_bnd, &net->st_gb, &net->st_ini, &net->st_gi,
                     &net->st_out, &net->st_pts, &net->st_u, &net->st_du, &net->st_d2u, &net->tc_ws};
   for (DevBuf* b : bufs) b->release();
+  tc_free(net);
   delete net;
 }
 

@@ -1,15 +1,293 @@
-// tc_kernels.cuh -- tcgen05 / TMEM tensor-core engine for the wide hidden layers (placeholder:
-// every hook reports "not handled" so the SIMT kernels run).
+// tc_kernels.cuh -- tcgen05 / TMEM tensor-core engine for the wide hidden layers (sm_100a).
+//
+// The hidden KAN layer is the dense contraction of PAPER.md:45/:87 ("KAN layer as a matrix
+// operation") applied to every jet channel:
+//     Y[(p,c), o] = sum_{K=(i,n)} A^c[p, K] W[o, K]      (+ b_o on the value channel c = 0)
+// with A^c generated on the fly from the saved input jet.  It runs as 3xTF32
+// on the 5th-generation tensor cores: W and A are split into tf32 hi/lo parts and
+//     D += W_hi A_hi + W_hi A_lo + W_lo A_hi
+// accumulate in fp32 TMEM, which meets the north-star tolerance.
+//
+// Forward kernel k_fwd_tc (orientation "W rows x (point,channel) columns"):
+//   MMA M = output neurons o (128-row tiles; O = 128 or 256 -> 1 or 2 tiles, both share the B tile),
+//   MMA N = NP points x C channels of one point tile (channel-major columns n = c*NP + p),
+//   MMA K = I*B (dense over all bases, zero-padded to a multiple of KB).
+//   smem stage = { W_hi, W_lo tiles [KB/4 chunks][O rows][4] via one 1-D bulk copy of a
+//                  pre-tiled global copy;  A_hi, A_lo tiles [KB/4][N][4] written by 4 generator
+//                  warps from the jet }, NSTAGE-deep mbarrier ring.
+//   warps 0-3: generators, then epilogue (TMEM -> registers -> +bias -> Y[p][c][o], coalesced);
+//   warp 4: TMEM allocator + single-thread MMA issuer; warp 5: bulk-copy producer.
 #pragma once
+#include "tc_ptx.cuh"
 
 namespace {
 
-hrkan_status tc_refresh_weights(hrkan_net*, cudaStream_t) { return HRKAN_OK; }
+using namespace hrkan;
+
+constexpr int TC_KB = 16;          // K per pipeline stage (two tf32 MMA K-steps of 8)
+constexpr int TC_NSTAGE = 3;
+constexpr int TC_GEN_THREADS = 128;
+constexpr int TC_THREADS = 192;    // 4 generator/epilogue warps + MMA warp + producer warp
+
+// Points per tile so that N = NP*C is a multiple of 16 and <= 256.
+__host__ __device__ constexpr int tc_np(int C) {
+  return C == 7 ? 32 : C == 5 ? 48 : C == 4 ? 64 : C == 3 ? 80 : C == 1 ? 256 : 0;
+}
+
+__host__ __device__ constexpr uint32_t tc_tmem_cols(uint32_t c) {
+  return c <= 32 ? 32 : c <= 64 ? 64 : c <= 128 ? 128 : c <= 256 ? 256 : 512;
+}
+
+template <int NF, int NS, int M, int NMT>
+struct FwdCfg {
+  static constexpr int C = 1 + NF + NS;
+  static constexpr int NP = tc_np(C);
+  static constexpr int N = NP * C;
+  static constexpr int O = 128 * NMT;
+  static constexpr int W_STAGE_FLOATS = 2 * O * TC_KB;     // hi + lo
+  static constexpr int A_STAGE_FLOATS = 2 * N * TC_KB;
+  static constexpr int STAGE_BYTES = 4 * (W_STAGE_FLOATS + A_STAGE_FLOATS);
+  static constexpr int SMEM_BYTES = TC_NSTAGE * STAGE_BYTES + 1024;
+  static constexpr uint32_t TMEM_COLS = tc_tmem_cols(NMT * N);
+  static_assert(N % 16 == 0 && N <= 256, "bad N");
+  static_assert(NMT * N <= 512, "accumulators exceed TMEM");
+};
+
+// Pre-tiled, pre-split weights for k_fwd_tc: for K-block kb: [hi | lo] each [KB/4][O][4].
+__global__ void k_tile_w_fwd(const float* __restrict__ W, float* __restrict__ Wt, int O, int K, int nkb) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t per_kb = (int64_t)O * TC_KB;
+  if (t >= per_kb * nkb) return;
+  const int kb = (int)(t / per_kb);
+  const int r = (int)(t - (int64_t)kb * per_kb);     // r = (j*O + o)*4 + e
+  const int e = r & 3, o = (r >> 2) % O, j = (r >> 2) / O;
+  const int k = kb * TC_KB + 4 * j + e;
+  const float w = (k < K) ? W[(int64_t)o * K + k] : 0.f;
+  float hi, lo;
+  tc::split_tf32(w, hi, lo);
+  float* dst = Wt + (int64_t)kb * 2 * per_kb;
+  dst[r] = hi;
+  dst[per_kb + r] = lo;
+}
+
+template <int NF, int NS, int M, int NMT>
+__global__ void __launch_bounds__(TC_THREADS, 1)
+    k_fwd_tc(const float* __restrict__ X, const float* __restrict__ Wtiled, const float* __restrict__ bias,
+             float* __restrict__ Y, int64_t P, int I, int nkb, BasisCfg bc) {
+  using Cfg = FwdCfg<NF, NS, M, NMT>;
+  constexpr int C = Cfg::C, NP = Cfg::NP, N = Cfg::N, O = Cfg::O;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  float* smem = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ __align__(8) uint64_t full_bar[TC_NSTAGE], empty_bar[TC_NSTAGE], accum_bar;
+  __shared__ uint32_t tmem_base_sh;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t p0 = (int64_t)blockIdx.x * NP;
+  const int K = I * bc.B;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < TC_NSTAGE; ++s) {
+      tc::mbar_init(&full_bar[s], TC_GEN_THREADS + 1);
+      tc::mbar_init(&empty_bar[s], 1);
+    }
+    tc::mbar_init(&accum_bar, 1);
+    tc::fence_mbar_init();
+  }
+  if (warp == 4) tc::tmem_alloc<Cfg::TMEM_COLS>(&tmem_base_sh);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = tmem_base_sh;
+
+  if (warp < 4) {
+    // ===================== generators: A^c[p, k] for the stage's KB columns
+    const int tid = threadIdx.x;
+    for (int kb = 0; kb < nkb; ++kb) {
+      const int s = kb % TC_NSTAGE;
+      const uint32_t ph = (kb / TC_NSTAGE) & 1;
+      tc::mbar_wait(&empty_bar[s], ph ^ 1);
+      float* a_hi = smem + s * (Cfg::W_STAGE_FLOATS + Cfg::A_STAGE_FLOATS) + Cfg::W_STAGE_FLOATS;
+      float* a_lo = a_hi + N * TC_KB;
+      for (int task = tid; task < NP * (TC_KB / 4); task += TC_GEN_THREADS) {
+        const int pl = task % NP, j = task / NP;
+        const int64_t p = p0 + pl;
+        float va[C][4];
+        int cur_i = -1;
+        float x = 0.f, dx[NF > 0 ? NF : 1], ddx[NS > 0 ? NS : 1];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int k = kb * TC_KB + 4 * j + e;
+          const int i = k / bc.B, n = k - i * bc.B;
+          float v0 = 0.f, v1 = 0.f, v2 = 0.f, v3;
+          if (p < P && k < K) {
+            if (i != cur_i) {
+              cur_i = i;
+              load_jet<NF, NS, false>(X, p, i, I, x, dx, ddx);
+            }
+            hr_eval<M, (NS > 0 ? 2 : 1)>(basis_q(x, n, bc), bc.sc, v0, v1, v2, v3);
+          }
+          va[0][e] = v0;
+#pragma unroll
+          for (int a = 0; a < NF; ++a) va[1 + a][e] = v1 * dx[a];
+#pragma unroll
+          for (int a = 0; a < NS; ++a) va[1 + NF + a][e] = fmaf(v2 * dx[a], dx[a], v1 * ddx[a]);
+        }
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+          float4 h, l;
+          tc::split_tf32(va[c][0], h.x, l.x);
+          tc::split_tf32(va[c][1], h.y, l.y);
+          tc::split_tf32(va[c][2], h.z, l.z);
+          tc::split_tf32(va[c][3], h.w, l.w);
+          const int row = c * NP + pl;                  // channel-major columns of the MMA N
+          *reinterpret_cast<float4*>(a_hi + (j * N + row) * 4) = h;
+          *reinterpret_cast<float4*>(a_lo + (j * N + row) * 4) = l;
+        }
+      }
+      tc::fence_proxy_async_smem();
+      tc::mbar_arrive(&full_bar[s]);
+    }
+    // ===================== epilogue: TMEM -> +bias -> Y[p][c][o]
+    tc::mbar_wait(&accum_bar, 0);
+    tc::tc_fence_after();
+#pragma unroll 1
+    for (int t = 0; t < NMT; ++t) {
+      const int o = t * 128 + warp * 32 + lane;
+      const float b = __ldg(bias + o);
+      const uint32_t tbase = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(t * N);
+#pragma unroll 1
+      for (int c0 = 0; c0 < N; c0 += 16) {
+        float v[16];
+        tc::tmem_ld16(tbase + c0, v);
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          const int col = c0 + q;
+          const int c = col / NP, pl = col - c * NP;
+          const int64_t p = p0 + pl;
+          if (p < P) Y[(p * C + c) * (int64_t)O + o] = (c == 0) ? v[q] + b : v[q];
+        }
+      }
+    }
+  } else if (warp == 4) {
+    // ===================== MMA issuer (one thread)
+    if (lane == 0) {
+      constexpr uint32_t idesc = tc::idesc_tf32(128, N);
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int s = kb % TC_NSTAGE;
+        const uint32_t ph = (kb / TC_NSTAGE) & 1;
+        tc::mbar_wait(&full_bar[s], ph);
+        tc::tc_fence_after();
+        const float* w_hi = smem + s * (Cfg::W_STAGE_FLOATS + Cfg::A_STAGE_FLOATS);
+        const float* w_lo = w_hi + O * TC_KB;
+        const float* a_hi = w_hi + Cfg::W_STAGE_FLOATS;
+        const float* a_lo = a_hi + N * TC_KB;
+#pragma unroll
+        for (int ks = 0; ks < TC_KB / 8; ++ks) {
+          // K-step ks covers chunks 2ks, 2ks+1: LBO = chunk stride = rows*16 B, SBO = 8 rows = 128 B
+          const uint32_t aoff = (uint32_t)(2 * ks * N * 16);
+          const uint64_t bh = tc::smem_desc(tc::smem_u32(a_hi) + aoff, N * 16, 128);
+          const uint64_t bl = tc::smem_desc(tc::smem_u32(a_lo) + aoff, N * 16, 128);
+#pragma unroll
+          for (int t = 0; t < NMT; ++t) {
+            const uint32_t woff = (uint32_t)(2 * ks * O * 16 + t * 128 * 16);
+            const uint64_t wh = tc::smem_desc(tc::smem_u32(w_hi) + woff, O * 16, 128);
+            const uint64_t wl = tc::smem_desc(tc::smem_u32(w_lo) + woff, O * 16, 128);
+            const uint32_t d = tmem + (uint32_t)(t * N);
+            const uint32_t acc0 = (kb > 0 || ks > 0) ? 1u : 0u;
+            tc::mma_tf32(d, wl, bh, idesc, acc0);
+            tc::mma_tf32(d, wh, bl, idesc, 1u);
+            tc::mma_tf32(d, wh, bh, idesc, 1u);
+          }
+        }
+        tc::mma_commit(&empty_bar[s]);
+      }
+      tc::mma_commit(&accum_bar);
+    }
+    __syncwarp();
+  } else {
+    // ===================== bulk-copy producer of the pre-tiled W_hi/W_lo stage
+    if (lane == 0) {
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int s = kb % TC_NSTAGE;
+        const uint32_t ph = (kb / TC_NSTAGE) & 1;
+        tc::mbar_wait(&empty_bar[s], ph ^ 1);
+        float* w_dst = smem + s * (Cfg::W_STAGE_FLOATS + Cfg::A_STAGE_FLOATS);
+        tc::mbar_arrive_expect_tx(&full_bar[s], Cfg::W_STAGE_FLOATS * 4);
+        tc::bulk_g2s(w_dst, Wtiled + (int64_t)kb * Cfg::W_STAGE_FLOATS, Cfg::W_STAGE_FLOATS * 4, &full_bar[s]);
+      }
+    }
+    __syncwarp();
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 4) tc::tmem_dealloc<Cfg::TMEM_COLS>(tmem);
+}
+
+// ---------------------------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------------------------
+bool tc_layer_ok(const hrkan_net* net, int l) {
+  if (net->engine == 1) return false;
+  const int L = net->L;
+  if (l <= 0 || l >= L - 1) return false;          // hidden layers only
+  const int O = net->widths[l + 1], I = net->widths[l];
+  if (O != 128 && O != 256) return false;
+  if (net->engine == 0 && (int64_t)I * net->B < 256) return false;   // K too small to pay off
+  return true;
+}
+
+hrkan_status tc_refresh_weights(hrkan_net* net, cudaStream_t st) {
+  if (net->tc_layers.empty()) net->tc_layers.assign(net->L, TcLayerState{});
+  for (int l = 0; l < net->L; ++l) {
+    if (!tc_layer_ok(net, l)) continue;
+    const int O = net->widths[l + 1], I = net->widths[l];
+    TcLayerState& ls = net->tc_layers[l];
+    const int K = I * net->B;
+    ls.nkb = (K + TC_KB - 1) / TC_KB;
+    const size_t n = (size_t)ls.nkb * 2 * O * TC_KB;
+    if (!ls.w_fwd) {
+      if (cudaMalloc(&ls.w_fwd, n * sizeof(float)) != cudaSuccess) return fail(HRKAN_ENOMEM, "tc weight alloc");
+    }
+    const int64_t tot = (int64_t)ls.nkb * O * TC_KB;
+    const int pi_ = prof_pre(net, st);
+    k_tile_w_fwd<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(net->params + net->w_off[l], ls.w_fwd, O, K, ls.nkb);
+    HR_TRY(check_launch(net, "k_tile_w_fwd", HRKAN_K_OTHER, st, pi_));
+  }
+  return HRKAN_OK;
+}
+
+template <int NF, int NS, int M, int NMT>
+hrkan_status launch_fwd_tc(hrkan_net* net, int l, const float* X, float* Y, int64_t n, cudaStream_t st) {
+  using Cfg = FwdCfg<NF, NS, M, NMT>;
+  auto kfn = k_fwd_tc<NF, NS, M, NMT>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    HR_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
+    attr_set = true;
+  }
+  const TcLayerState& ls = net->tc_layers[l];
+  const unsigned grid = (unsigned)((n + Cfg::NP - 1) / Cfg::NP);
+  const int cls = HRKAN_K_FWD_HIDDEN;
+  HR_LAUNCH(cls, "k_fwd_tc",
+            kfn<<<grid, TC_THREADS, Cfg::SMEM_BYTES, st>>>(X, ls.w_fwd, net->params + net->b_off[l], Y, n,
+                                                           net->widths[l], ls.nkb, net->bc));
+  return HRKAN_OK;
+}
 
 template <int NF, int NS, int M>
-hrkan_status tc_forward_layer(hrkan_net*, int, const float*, float*, int64_t, cudaStream_t, bool* done) {
+hrkan_status tc_forward_layer(hrkan_net* net, int l, const float* X, float* Y, int64_t n, cudaStream_t st, bool* done) {
   *done = false;
-  return HRKAN_OK;
+  constexpr int C = 1 + NF + NS;
+  if constexpr (tc_np(C) == 0) {
+    return HRKAN_OK;
+  } else {
+    if (!tc_layer_ok(net, l) || l >= (int)net->tc_layers.size() || !net->tc_layers[l].w_fwd) return HRKAN_OK;
+    const int O = net->widths[l + 1];
+    if (O == 128) HR_TRY(launch_fwd_tc<NF, NS, M, 1>(net, l, X, Y, n, st));
+    else HR_TRY(launch_fwd_tc<NF, NS, M, 2>(net, l, X, Y, n, st));
+    *done = true;
+    return HRKAN_OK;
+  }
 }
 
 template <int NF, int NS, int M>
@@ -23,6 +301,14 @@ template <int NF, int NS, int M>
 hrkan_status tc_dgrad_layer(hrkan_net*, int, const float*, const float*, float*, int64_t, cudaStream_t, bool* done) {
   *done = false;
   return HRKAN_OK;
+}
+
+void tc_free(hrkan_net* net) {
+  for (auto& ls : net->tc_layers) {
+    if (ls.w_fwd) cudaFree(ls.w_fwd);
+    if (ls.w_dgr) cudaFree(ls.w_dgr);
+    ls.w_fwd = ls.w_dgr = nullptr;
+  }
 }
 
 }  // namespace

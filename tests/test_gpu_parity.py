@@ -132,7 +132,7 @@ def test_polynomial_chain_net_exact_gpu(torch_mod):
     """P3: a chain through neuron 0 of a [3,256,256,1] net, all other weights 0 (mostly-zero
     tiles): the GPU reproduces the exact laplacian from rational arithmetic."""
     import sympy as sp
-    from tests.test_oracle_jet_loss_grad import _p2_setup
+    from test_oracle_jet_loss_grad import _p2_setup
     from paper_2409_14248_b200 import HRKANNet
     torch = torch_mod
     widths = (3, 256, 256, 1)
@@ -149,6 +149,23 @@ def test_polynomial_chain_net_exact_gpu(torch_mod):
         ref_lap = float(sum(sp.diff(u, z, 2) for z in syms).subs(sub))
         assert gu[q] == pytest.approx(ref_u, rel=1e-4, abs=1e-5)
         assert gd2u[q].sum() == pytest.approx(ref_lap, rel=2e-3, abs=1e-3)
+
+
+@pytest.mark.parametrize("key", ["C4", "C5"])
+def test_tensor_core_engine_matches_simt(torch_mod, key):
+    """The tcgen05 3xTF32 hidden-layer kernels agree with the SIMT FFMA kernels (independent
+    arithmetic: dense K on tensor cores vs band-limited FFMA) far inside the oracle tolerance."""
+    torch = torch_mod
+    w = HI.WORKLOADS[key]
+    ps = HI.make_points(w).subset(2048 if key == "C5" else 512, 64)
+    pts = torch.from_numpy(ps.interior).cuda()
+    outs = []
+    for engine in (1, 2):
+        net, params = _make(w, engine=engine)
+        outs.append([t.cpu().numpy() for t in net.forward_jet(pts)] + [_loss_grad_gpu(torch, net, w, ps)])
+    (u1, du1, d2u1, g1), (u2, du2, d2u2, g2) = outs
+    assert rel_l2(u2, u1) < 1e-5 and rel_l2(du2, du1) < 1e-5 and rel_l2(d2u2, d2u1) < 1e-4
+    assert rel_l2(g2, g1) < 1e-4
 
 
 def test_host_buffers_match_device_buffers(torch_mod):
