@@ -124,6 +124,7 @@ struct hrkan_net {
   DevBuf st_int, st_f, st_bnd, st_gb, st_ini, st_gi, st_out, st_pts, st_u, st_du, st_d2u;
   DevBuf tc_ws;                         // tensor-core path scratch
   std::vector<TcLayerState> tc_layers;
+  int tc_seg = 32;                      // K-blocks per TMEM accumulation segment (precision bound)
   // device-time profiling (hrkan_profile_enable / hrkan_profile_read)
   struct ProfEv { cudaEvent_t a, b; int cls; };
   bool prof_on = false;

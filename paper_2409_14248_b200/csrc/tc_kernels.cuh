@@ -48,7 +48,8 @@ struct FwdCfg {
   static constexpr int A_STAGE_FLOATS = 2 * N * TC_KB;
   static constexpr int STAGE_BYTES = 4 * (W_STAGE_FLOATS + A_STAGE_FLOATS);
   static constexpr int SMEM_BYTES = TC_NSTAGE * STAGE_BYTES + 1024;
-  static constexpr uint32_t TMEM_COLS = tc_tmem_cols(NMT * N);
+  static constexpr int NACC = (2 * NMT * N <= 512) ? 2 : 1;   // double-buffered accumulators if they fit
+  static constexpr uint32_t TMEM_COLS = tc_tmem_cols(NACC * NMT * N);
   static_assert(N % 16 == 0 && N <= 256, "bad N");
   static_assert(NMT * N <= 512, "accumulators exceed TMEM");
 };
@@ -73,24 +74,28 @@ __global__ void k_tile_w_fwd(const float* __restrict__ W, float* __restrict__ Wt
 template <int NF, int NS, int M, int NMT>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     k_fwd_tc(const float* __restrict__ X, const float* __restrict__ Wtiled, const float* __restrict__ bias,
-             float* __restrict__ Y, int64_t P, int I, int nkb, BasisCfg bc) {
+             float* __restrict__ Y, int64_t P, int I, int nkb, int seg, BasisCfg bc) {
   using Cfg = FwdCfg<NF, NS, M, NMT>;
-  constexpr int C = Cfg::C, NP = Cfg::NP, N = Cfg::N, O = Cfg::O;
+  constexpr int C = Cfg::C, NP = Cfg::NP, N = Cfg::N, O = Cfg::O, NACC = Cfg::NACC;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   float* smem = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ __align__(8) uint64_t full_bar[TC_NSTAGE], empty_bar[TC_NSTAGE], accum_bar;
+  __shared__ __align__(8) uint64_t full_bar[TC_NSTAGE], empty_bar[TC_NSTAGE], acc_full[NACC], acc_empty[NACC];
   __shared__ uint32_t tmem_base_sh;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t p0 = (int64_t)blockIdx.x * NP;
   const int K = I * bc.B;
+  const int nseg = (nkb + seg - 1) / seg;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < TC_NSTAGE; ++s) {
       tc::mbar_init(&full_bar[s], TC_GEN_THREADS + 1);
       tc::mbar_init(&empty_bar[s], 1);
     }
-    tc::mbar_init(&accum_bar, 1);
+    for (int a = 0; a < NACC; ++a) {
+      tc::mbar_init(&acc_full[a], 1);
+      tc::mbar_init(&acc_empty[a], TC_GEN_THREADS);
+    }
     tc::fence_mbar_init();
   }
   if (warp == 4) tc::tmem_alloc<Cfg::TMEM_COLS>(&tmem_base_sh);
@@ -100,9 +105,42 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const uint32_t tmem = tmem_base_sh;
 
   if (warp < 4) {
+    // Drain K-segment sg: TMEM accumulator -> Y (first segment: = D + bias; later: += D), fp32 RN.
+    // Bounds the tensor core's accumulation error to one segment.
+    auto drain = [&](int sg) {
+      const int buf = sg % NACC;
+      tc::mbar_wait(&acc_full[buf], (uint32_t)((sg / NACC) & 1));
+      tc::tc_fence_after();
+#pragma unroll 1
+      for (int t = 0; t < NMT; ++t) {
+        const int o = t * 128 + warp * 32 + lane;
+        const float b = (sg == 0) ? __ldg(bias + o) : 0.f;
+        const uint32_t tbase = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)((buf * NMT + t) * N);
+#pragma unroll 1
+        for (int c0 = 0; c0 < N; c0 += 16) {
+          float v[16];
+          tc::tmem_ld16(tbase + c0, v);
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            const int col = c0 + q;
+            const int c = col / NP, pl = col - c * NP;
+            const int64_t p = p0 + pl;
+            if (p < P) {
+              float* y = Y + (p * C + c) * (int64_t)O + o;
+              if (sg == 0) *y = (c == 0) ? v[q] + b : v[q];
+              else *y += v[q];
+            }
+          }
+        }
+      }
+      tc::tc_fence_before();
+      tc::mbar_arrive(&acc_empty[buf]);
+    };
     // ===================== generators: A^c[p, k] for the stage's KB columns
     const int tid = threadIdx.x;
+    int next_drain = 0;
     for (int kb = 0; kb < nkb; ++kb) {
+      while (next_drain < nseg - 1 && kb >= (next_drain + 1) * seg + TC_NSTAGE) drain(next_drain++);
       const int s = kb % TC_NSTAGE;
       const uint32_t ph = (kb / TC_NSTAGE) & 1;
       tc::mbar_wait(&empty_bar[s], ph ^ 1);
@@ -147,32 +185,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       tc::fence_proxy_async_smem();
       tc::mbar_arrive(&full_bar[s]);
     }
-    // ===================== epilogue: TMEM -> +bias -> Y[p][c][o]
-    tc::mbar_wait(&accum_bar, 0);
-    tc::tc_fence_after();
-#pragma unroll 1
-    for (int t = 0; t < NMT; ++t) {
-      const int o = t * 128 + warp * 32 + lane;
-      const float b = __ldg(bias + o);
-      const uint32_t tbase = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(t * N);
-#pragma unroll 1
-      for (int c0 = 0; c0 < N; c0 += 16) {
-        float v[16];
-        tc::tmem_ld16(tbase + c0, v);
-#pragma unroll
-        for (int q = 0; q < 16; ++q) {
-          const int col = c0 + q;
-          const int c = col / NP, pl = col - c * NP;
-          const int64_t p = p0 + pl;
-          if (p < P) Y[(p * C + c) * (int64_t)O + o] = (c == 0) ? v[q] + b : v[q];
-        }
-      }
-    }
+    while (next_drain < nseg) drain(next_drain++);
   } else if (warp == 4) {
     // ===================== MMA issuer (one thread)
     if (lane == 0) {
       constexpr uint32_t idesc = tc::idesc_tf32(128, N);
       for (int kb = 0; kb < nkb; ++kb) {
+        const int sg = kb / seg, buf = sg % NACC;
+        const bool seg_first = (kb % seg) == 0;
+        if (seg_first && sg >= NACC) {
+          tc::mbar_wait(&acc_empty[buf], (uint32_t)((sg / NACC - 1) & 1));
+          tc::tc_fence_after();
+        }
         const int s = kb % TC_NSTAGE;
         const uint32_t ph = (kb / TC_NSTAGE) & 1;
         tc::mbar_wait(&full_bar[s], ph);
@@ -192,16 +216,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             const uint32_t woff = (uint32_t)(2 * ks * O * 16 + t * 128 * 16);
             const uint64_t wh = tc::smem_desc(tc::smem_u32(w_hi) + woff, O * 16, 128);
             const uint64_t wl = tc::smem_desc(tc::smem_u32(w_lo) + woff, O * 16, 128);
-            const uint32_t d = tmem + (uint32_t)(t * N);
-            const uint32_t acc0 = (kb > 0 || ks > 0) ? 1u : 0u;
+            const uint32_t d = tmem + (uint32_t)((buf * NMT + t) * N);
+            const uint32_t acc0 = (seg_first && ks == 0) ? 0u : 1u;
             tc::mma_tf32(d, wl, bh, idesc, acc0);
             tc::mma_tf32(d, wh, bl, idesc, 1u);
             tc::mma_tf32(d, wh, bh, idesc, 1u);
           }
         }
         tc::mma_commit(&empty_bar[s]);
+        if ((kb % seg) == seg - 1 || kb == nkb - 1) tc::mma_commit(&acc_full[buf]);
       }
-      tc::mma_commit(&accum_bar);
     }
     __syncwarp();
   } else {
@@ -270,7 +294,7 @@ hrkan_status launch_fwd_tc(hrkan_net* net, int l, const float* X, float* Y, int6
   const int cls = HRKAN_K_FWD_HIDDEN;
   HR_LAUNCH(cls, "k_fwd_tc",
             kfn<<<grid, TC_THREADS, Cfg::SMEM_BYTES, st>>>(X, ls.w_fwd, net->params + net->b_off[l], Y, n,
-                                                           net->widths[l], ls.nkb, net->bc));
+                                                           net->widths[l], ls.nkb, net->tc_seg, net->bc));
   return HRKAN_OK;
 }
 
