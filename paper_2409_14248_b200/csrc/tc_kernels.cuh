@@ -26,8 +26,10 @@ using namespace hrkan;
 
 constexpr int TC_KB = 16;          // K per pipeline stage (two tf32 MMA K-steps of 8)
 constexpr int TC_NSTAGE = 3;
-constexpr int TC_GEN_THREADS = 128;
-constexpr int TC_THREADS = 192;    // 4 generator/epilogue warps + MMA warp + producer warp
+constexpr int TC_GEN_THREADS = 128;   // one generator group (4 warps); the group handles every other K-block
+constexpr int TC_NGEN = 2;            // generator groups (group 0 also drains the accumulators)
+constexpr int TC_THREADS = 32 * (4 * TC_NGEN + 2);   // + MMA warp + producer warp
+constexpr int TC_MMA_WARP = 4 * TC_NGEN, TC_PROD_WARP = 4 * TC_NGEN + 1;
 
 // Points per tile so that N = NP*C is a multiple of 16 and <= 256.
 __host__ __device__ constexpr int tc_np(int C) {
@@ -94,17 +96,20 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
     for (int a = 0; a < NACC; ++a) {
       tc::mbar_init(&acc_full[a], 1);
-      tc::mbar_init(&acc_empty[a], TC_GEN_THREADS);
+      tc::mbar_init(&acc_empty[a], TC_GEN_THREADS * TC_NGEN);
     }
     tc::fence_mbar_init();
   }
-  if (warp == 4) tc::tmem_alloc<Cfg::TMEM_COLS>(&tmem_base_sh);
+  if (warp == TC_MMA_WARP) tc::tmem_alloc<Cfg::TMEM_COLS>(&tmem_base_sh);
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem = tmem_base_sh;
 
-  if (warp < 4) {
+  if (warp < 4 * TC_NGEN) {
+    const int grp = warp >> 2;                 // generator group: K-blocks kb = grp (mod TC_NGEN)
+    const int gtid = threadIdx.x & (TC_GEN_THREADS - 1);
+    const int qw = warp & 3;                   // TMEM lane quadrant of this warp
     // Drain K-segment sg: TMEM accumulator -> Y (first segment: = D + bias; later: += D), fp32 RN.
     // Bounds the tensor core's accumulation error to one segment.
     auto drain = [&](int sg) {
@@ -113,80 +118,135 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       tc::tc_fence_after();
 #pragma unroll 1
       for (int t = 0; t < NMT; ++t) {
-        const int o = t * 128 + warp * 32 + lane;
+        const int o = t * 128 + qw * 32 + lane;
         const float b = (sg == 0) ? __ldg(bias + o) : 0.f;
-        const uint32_t tbase = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)((buf * NMT + t) * N);
+        const uint32_t tbase = tmem + ((uint32_t)(qw * 32) << 16) + (uint32_t)((buf * NMT + t) * N);
+        // 16-column chunks are shared round-robin by the generator groups (same lane quadrant)
 #pragma unroll 1
-        for (int c0 = 0; c0 < N; c0 += 16) {
+        for (int c0 = 16 * grp; c0 < N; c0 += 16 * TC_NGEN) {
           float v[16];
           tc::tmem_ld16(tbase + c0, v);
+          float* yp[16];
+          bool ok[16];
 #pragma unroll
           for (int q = 0; q < 16; ++q) {
             const int col = c0 + q;
             const int c = col / NP, pl = col - c * NP;
             const int64_t p = p0 + pl;
-            if (p < P) {
-              float* y = Y + (p * C + c) * (int64_t)O + o;
-              if (sg == 0) *y = (c == 0) ? v[q] + b : v[q];
-              else *y += v[q];
-            }
+            ok[q] = p < P;
+            yp[q] = Y + (p * C + c) * (int64_t)O + o;
+            if (sg == 0 && c == 0) v[q] += b;
           }
+          if (sg > 0) {
+            float old[16];
+#pragma unroll
+            for (int q = 0; q < 16; ++q) old[q] = ok[q] ? *yp[q] : 0.f;   // 16 loads in flight
+#pragma unroll
+            for (int q = 0; q < 16; ++q) v[q] += old[q];
+          }
+#pragma unroll
+          for (int q = 0; q < 16; ++q)
+            if (ok[q]) *yp[q] = v[q];
         }
       }
       tc::tc_fence_before();
       tc::mbar_arrive(&acc_empty[buf]);
     };
-    // ===================== generators: A^c[p, k] for the stage's KB columns
-    const int tid = threadIdx.x;
+    // ===================== generators: A^c[p, k] for the stage's KB columns.
+    // Each thread owns TPT tasks (point pl, 4-wide K chunk j) per block; the jets of the next
+    // block are prefetched into registers while the current block is generated.
+    constexpr int NTASK = NP * (TC_KB / 4);
+    constexpr int TPT = (NTASK + TC_GEN_THREADS - 1) / TC_GEN_THREADS;
+    float jx[2][TPT][2], jdx[2][TPT][2][NF > 0 ? NF : 1], jddx[2][TPT][2][NS > 0 ? NS : 1];
+    auto prefetch = [&](int kb, auto SLOT) {
+      constexpr int slot = decltype(SLOT)::value;
+#pragma unroll
+      for (int u = 0; u < TPT; ++u) {
+        const int task = gtid + u * TC_GEN_THREADS;
+        const int pl = task % NP, j = task / NP;
+        const int64_t p = p0 + pl;
+        const int k0 = kb * TC_KB + 4 * j;
+        const int i0 = k0 / bc.B;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int i = i0 + h;
+          jx[slot][u][h] = 0.f;
+#pragma unroll
+          for (int a = 0; a < NF; ++a) jdx[slot][u][h][a] = 0.f;
+#pragma unroll
+          for (int a = 0; a < NS; ++a) jddx[slot][u][h][a] = 0.f;
+          if (task < NTASK && p < P && i < I && kb < nkb) {
+            const float* base = X + p * (int64_t)(C * I) + i;
+            jx[slot][u][h] = __ldg(base);
+#pragma unroll
+            for (int a = 0; a < NF; ++a) jdx[slot][u][h][a] = __ldg(base + (1 + a) * I);
+#pragma unroll
+            for (int a = 0; a < NS; ++a) jddx[slot][u][h][a] = __ldg(base + (1 + NF + a) * I);
+          }
+        }
+      }
+    };
     int next_drain = 0;
-    for (int kb = 0; kb < nkb; ++kb) {
+    // one K-block: prefetch the group's next block into the other register slot, then generate
+    auto step = [&](int kb, auto SLOT) {
+      constexpr int slot = decltype(SLOT)::value;
       while (next_drain < nseg - 1 && kb >= (next_drain + 1) * seg + TC_NSTAGE) drain(next_drain++);
+      prefetch(kb + TC_NGEN, std::integral_constant<int, slot ^ 1>{});
       const int s = kb % TC_NSTAGE;
       const uint32_t ph = (kb / TC_NSTAGE) & 1;
       tc::mbar_wait(&empty_bar[s], ph ^ 1);
       float* a_hi = smem + s * (Cfg::W_STAGE_FLOATS + Cfg::A_STAGE_FLOATS) + Cfg::W_STAGE_FLOATS;
       float* a_lo = a_hi + N * TC_KB;
-      for (int task = tid; task < NP * (TC_KB / 4); task += TC_GEN_THREADS) {
+#pragma unroll
+      for (int u = 0; u < TPT; ++u) {
+        const int task = gtid + u * TC_GEN_THREADS;
+        if (task >= NTASK) break;
         const int pl = task % NP, j = task / NP;
-        const int64_t p = p0 + pl;
+        const int k0 = kb * TC_KB + 4 * j;
+        const int i0 = k0 / bc.B;
+        int n = k0 - i0 * bc.B;
         float va[C][4];
-        int cur_i = -1;
-        float x = 0.f, dx[NF > 0 ? NF : 1], ddx[NS > 0 ? NS : 1];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          const int k = kb * TC_KB + 4 * j + e;
-          const int i = k / bc.B, n = k - i * bc.B;
-          float v0 = 0.f, v1 = 0.f, v2 = 0.f, v3;
-          if (p < P && k < K) {
-            if (i != cur_i) {
-              cur_i = i;
-              load_jet<NF, NS, false>(X, p, i, I, x, dx, ddx);
-            }
-            hr_eval<M, (NS > 0 ? 2 : 1)>(basis_q(x, n, bc), bc.sc, v0, v1, v2, v3);
-          }
+          const bool h = n >= bc.B;                   // chunk crosses into input i0+1
+          const int nn = h ? n - bc.B : n;
+          const float x = h ? jx[slot][u][1] : jx[slot][u][0];
+          float v0, v1, v2, v3;
+          hr_eval<M, (NS > 0 ? 2 : 1)>(basis_q(x, nn, bc), bc.sc, v0, v1, v2, v3);
+          if (k0 + e >= K) v0 = v1 = v2 = 0.f;
           va[0][e] = v0;
 #pragma unroll
-          for (int a = 0; a < NF; ++a) va[1 + a][e] = v1 * dx[a];
+          for (int a = 0; a < NF; ++a) va[1 + a][e] = v1 * (h ? jdx[slot][u][1][a] : jdx[slot][u][0][a]);
 #pragma unroll
-          for (int a = 0; a < NS; ++a) va[1 + NF + a][e] = fmaf(v2 * dx[a], dx[a], v1 * ddx[a]);
+          for (int a = 0; a < NS; ++a) {
+            const float d1 = h ? jdx[slot][u][1][a] : jdx[slot][u][0][a];
+            const float d2 = h ? jddx[slot][u][1][a] : jddx[slot][u][0][a];
+            va[1 + NF + a][e] = fmaf(v2 * d1, d1, v1 * d2);
+          }
+          ++n;
         }
 #pragma unroll
         for (int c = 0; c < C; ++c) {
-          float4 h, l;
-          tc::split_tf32(va[c][0], h.x, l.x);
-          tc::split_tf32(va[c][1], h.y, l.y);
-          tc::split_tf32(va[c][2], h.z, l.z);
-          tc::split_tf32(va[c][3], h.w, l.w);
+          float4 hh, ll;
+          tc::split_tf32(va[c][0], hh.x, ll.x);
+          tc::split_tf32(va[c][1], hh.y, ll.y);
+          tc::split_tf32(va[c][2], hh.z, ll.z);
+          tc::split_tf32(va[c][3], hh.w, ll.w);
           const int row = c * NP + pl;                  // channel-major columns of the MMA N
-          *reinterpret_cast<float4*>(a_hi + (j * N + row) * 4) = h;
-          *reinterpret_cast<float4*>(a_lo + (j * N + row) * 4) = l;
+          *reinterpret_cast<float4*>(a_hi + (j * N + row) * 4) = hh;
+          *reinterpret_cast<float4*>(a_lo + (j * N + row) * 4) = ll;
         }
       }
       tc::fence_proxy_async_smem();
       tc::mbar_arrive(&full_bar[s]);
+    };
+    prefetch(grp, std::integral_constant<int, 0>{});
+    for (int kb = grp; kb < nkb; kb += 2 * TC_NGEN) {
+      step(kb, std::integral_constant<int, 0>{});
+      if (kb + TC_NGEN < nkb) step(kb + TC_NGEN, std::integral_constant<int, 1>{});
     }
     while (next_drain < nseg) drain(next_drain++);
-  } else if (warp == 4) {
+  } else if (warp == TC_MMA_WARP) {
     // ===================== MMA issuer (one thread)
     if (lane == 0) {
       constexpr uint32_t idesc = tc::idesc_tf32(128, N);
@@ -244,7 +304,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   }
   tc::tc_fence_before();
   __syncthreads();
-  if (warp == 4) tc::tmem_dealloc<Cfg::TMEM_COLS>(tmem);
+  if (warp == TC_MMA_WARP) tc::tmem_dealloc<Cfg::TMEM_COLS>(tmem);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -257,6 +317,7 @@ bool tc_layer_ok(const hrkan_net* net, int l) {
   const int O = net->widths[l + 1], I = net->widths[l];
   if (O != 128 && O != 256) return false;
   if (net->engine == 0 && (int64_t)I * net->B < 256) return false;   // K too small to pay off
+  if (net->B < 4) return false;                   // a 4-wide K chunk spans at most 2 inputs
   return true;
 }
 
@@ -294,7 +355,7 @@ hrkan_status launch_fwd_tc(hrkan_net* net, int l, const float* X, float* Y, int6
   const int cls = HRKAN_K_FWD_HIDDEN;
   HR_LAUNCH(cls, "k_fwd_tc",
             kfn<<<grid, TC_THREADS, Cfg::SMEM_BYTES, st>>>(X, ls.w_fwd, net->params + net->b_off[l], Y, n,
-                                                           net->widths[l], ls.nkb, net->tc_seg, net->bc));
+                                                           net->widths[l], ls.nkb, Cfg::NACC == 2 ? net->tc_seg : 2 * net->tc_seg, net->bc));
   return HRKAN_OK;
 }
 
