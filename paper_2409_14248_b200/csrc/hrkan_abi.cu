@@ -125,6 +125,7 @@ struct hrkan_net {
   DevBuf tc_ws;                         // tensor-core path scratch
   std::vector<TcLayerState> tc_layers;
   int tc_seg = 32;                      // K-blocks per TMEM accumulation segment (precision bound)
+  int tc_wseg = 256;                    // wgrad stages per TMEM drain into the fp32 master
   // device-time profiling (hrkan_profile_enable / hrkan_profile_read)
   struct ProfEv { cudaEvent_t a, b; int cls; };
   bool prof_on = false;

@@ -1,0 +1,270 @@
+// tc_dgrad.cuh -- tensor-core input-adjoint kernel of a hidden layer, included by
+// tc_kernels.cuh.
+//
+//   Abar^c[p,(i,n)] = sum_o Ybar^c[p,o] W[o,(i,n)]                  (3xTF32 tcgen05, fp32 TMEM)
+// then the jet-chain epilogue (v1, v2, v3 = first/second/third x-derivatives of basis n at x_i):
+//   xbar    = sum_n [Abar^0 v1 + sum_a Abar^{1,a} v2 dx_a + sum_a Abar^{2,a} (v3 dx_a^2 + v2 ddx_a)]
+//   dxbar_a = sum_n [Abar^{1,a} v1 + 2 Abar^{2,a} v2 dx_a],     ddxbar_a = sum_n Abar^{2,a} v1
+//
+// Orientation: MMA M = rows (i,n) of an INPUT-ALIGNED tile (IPT = floor(128/B) whole inputs, so every
+// sum over n closes inside one tile), MMA N = (point, channel) columns p*C + c of NP points, MMA
+// K = o.  A = pre-tiled W^T hi/lo (one 1-D bulk copy per stage), B = Ybar hi/lo (loaded + split by
+// 4 generator warps, next block prefetched in registers).  Two TMEM accumulators: the 4 epilogue
+// warps drain M-tile t while the MMA runs t+1.  Epilogue: TMEM -> smem slice of SLICE_P points ->
+// each (point, input) gathers only the k+1 non-zero bases of its x -> Xbar[p][c][i].
+#pragma once
+
+namespace {
+
+__host__ __device__ constexpr int dgr_slice_p(int C) { return C == 1 ? 64 : 8; }
+
+template <int NF, int NS, int M, int OT>
+struct DgrCfg {
+  static constexpr int C = 1 + NF + NS;
+  static constexpr int NP = tc_np(C);
+  static constexpr int N = NP * C;
+  static constexpr int O = 128 * OT;
+  static constexpr int NKB = O / TC_KB;
+  static constexpr int W_STAGE_FLOATS = 2 * 128 * TC_KB;
+  static constexpr int Y_STAGE_FLOATS = 2 * N * TC_KB;
+  static constexpr int SLICE_P = dgr_slice_p(C);
+  static constexpr int S_FLOATS = SLICE_P * C * 128;
+  static constexpr int STAGE_BYTES = 4 * (W_STAGE_FLOATS + Y_STAGE_FLOATS);
+  static constexpr int NSTAGE = (4 * STAGE_BYTES + 4 * S_FLOATS + 1024 <= 220 * 1024) ? 4 : 3;
+  static constexpr int SMEM_BYTES = NSTAGE * STAGE_BYTES + 4 * S_FLOATS + 1024;
+  static constexpr uint32_t TMEM_COLS = tc_tmem_cols(2 * N);
+  static_assert(N % 16 == 0 && N <= 256, "bad N");
+  static_assert(NP % SLICE_P == 0 && (SLICE_P * C) % 8 == 0, "bad slice");
+};
+constexpr int DGR_THREADS = 32 * 10;   // 4 generator warps, 4 epilogue warps, MMA warp, producer warp
+constexpr int DGR_EPI_WARP0 = 4, DGR_MMA_WARP = 8;
+
+// W^T tiles for k_dgrad_tc: for M-tile mt (inputs mt*IPT ...), K-block kb (o = kb*KB ...):
+// [hi | lo] each [KB/4][128 rows][4], row = il*B + n (il < IPT), zero outside.
+__global__ void k_tile_w_dgr(const float* __restrict__ W, float* __restrict__ Wt, int O, int I, int B, int IPT,
+                             int nmt) {
+  const int nkb = O / TC_KB;
+  const int64_t per = 128 * TC_KB;
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= per * nkb * nmt) return;
+  const int64_t blk = t / per;
+  const int r4 = (int)(t - blk * per);             // (j*128 + row)*4 + e
+  const int mt = (int)(blk / nkb), kb = (int)(blk - (int64_t)mt * nkb);
+  const int e = r4 & 3, row = (r4 >> 2) & 127, j = r4 >> 9;
+  const int o = kb * TC_KB + 4 * j + e;
+  const int il = row / B, n = row - il * B, i = mt * IPT + il;
+  const float w = (il < IPT && i < I) ? W[((int64_t)o * I + i) * B + n] : 0.f;
+  float hi, lo;
+  tc::split_tf32(w, hi, lo);
+  float* dst = Wt + blk * 2 * per;
+  dst[r4] = hi;
+  dst[per + r4] = lo;
+}
+
+template <int NF, int NS, int M, int OT>
+__global__ void __launch_bounds__(DGR_THREADS, 1)
+    k_dgrad_tc(const float* __restrict__ X, const float* __restrict__ Ybar, const float* __restrict__ Wtiled,
+               float* __restrict__ Xbar, int64_t P, int I, int IPT, int nmt, BasisCfg bc) {
+  using Cfg = DgrCfg<NF, NS, M, OT>;
+  constexpr int C = Cfg::C, NP = Cfg::NP, N = Cfg::N, O = Cfg::O, NKB = Cfg::NKB, NSTAGE = Cfg::NSTAGE;
+  constexpr int SLICE_P = Cfg::SLICE_P;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  float* smem = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  float* S = smem + NSTAGE * (Cfg::W_STAGE_FLOATS + Cfg::Y_STAGE_FLOATS);
+  __shared__ __align__(8) uint64_t full_bar[NSTAGE], empty_bar[NSTAGE], acc_full[2], acc_empty[2];
+  __shared__ uint32_t tmem_base_sh;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t p0 = (int64_t)blockIdx.x * NP;
+  const int nblk = nmt * NKB;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NSTAGE; ++s) {
+      tc::mbar_init(&full_bar[s], TC_GEN_THREADS + 1);
+      tc::mbar_init(&empty_bar[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      tc::mbar_init(&acc_full[a], 1);
+      tc::mbar_init(&acc_empty[a], 128);
+    }
+    tc::fence_mbar_init();
+  }
+  if (warp == DGR_MMA_WARP) tc::tmem_alloc<Cfg::TMEM_COLS>(&tmem_base_sh);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = tmem_base_sh;
+
+  if (warp < 4) {
+    // ===================== generators: Ybar tile [N rows (p,c)][KB o] hi/lo, rows p*C + c
+    constexpr int NTASK = N * (TC_KB / 4);
+    constexpr int TPT = (NTASK + TC_GEN_THREADS - 1) / TC_GEN_THREADS;
+    const int tid = threadIdx.x;
+    float4 buf[2][TPT];
+    auto prefetch = [&](int g, auto SLOT) {
+      constexpr int sl = decltype(SLOT)::value;
+      const int kb = g % NKB;
+#pragma unroll
+      for (int u = 0; u < TPT; ++u) {
+        const int task = tid + u * TC_GEN_THREADS;
+        const int row = task % N, j = task / N;
+        const int pl = row / C, c = row - pl * C;
+        const int64_t p = p0 + pl;
+        buf[sl][u] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (task < NTASK && p < P && g < nblk)
+          buf[sl][u] = __ldg(reinterpret_cast<const float4*>(Ybar + (p * C + c) * (int64_t)O + kb * TC_KB + 4 * j));
+      }
+    };
+    auto step = [&](int g, auto SLOT) {
+      constexpr int sl = decltype(SLOT)::value;
+      prefetch(g + 1, std::integral_constant<int, sl ^ 1>{});
+      const int s = g % NSTAGE;
+      tc::mbar_wait(&empty_bar[s], ((g / NSTAGE) & 1) ^ 1);
+      float* y_hi = smem + s * (Cfg::W_STAGE_FLOATS + Cfg::Y_STAGE_FLOATS) + Cfg::W_STAGE_FLOATS;
+      float* y_lo = y_hi + N * TC_KB;
+#pragma unroll
+      for (int u = 0; u < TPT; ++u) {
+        const int task = tid + u * TC_GEN_THREADS;
+        if (task >= NTASK) break;
+        const int row = task % N, j = task / N;
+        float4 h, l;
+        tc::split_tf32(buf[sl][u].x, h.x, l.x);
+        tc::split_tf32(buf[sl][u].y, h.y, l.y);
+        tc::split_tf32(buf[sl][u].z, h.z, l.z);
+        tc::split_tf32(buf[sl][u].w, h.w, l.w);
+        *reinterpret_cast<float4*>(y_hi + (j * N + row) * 4) = h;
+        *reinterpret_cast<float4*>(y_lo + (j * N + row) * 4) = l;
+      }
+      tc::fence_proxy_async_smem();
+      tc::mbar_arrive(&full_bar[s]);
+    };
+    prefetch(0, std::integral_constant<int, 0>{});
+    for (int g = 0; g < nblk; g += 2) {
+      step(g, std::integral_constant<int, 0>{});
+      if (g + 1 < nblk) step(g + 1, std::integral_constant<int, 1>{});
+    }
+  } else if (warp < DGR_MMA_WARP) {
+    // ===================== epilogue: per M-tile, TMEM -> smem slices -> jet-chain gather
+    const int qw = warp - DGR_EPI_WARP0;          // TMEM lane quadrant (warp % 4)
+    const int etid = threadIdx.x - 32 * DGR_EPI_WARP0;
+    const int r = qw * 32 + lane;                 // accumulator row = il*B + n
+    for (int mt = 0; mt < nmt; ++mt) {
+      const int buf = mt & 1;
+      tc::mbar_wait(&acc_full[buf], (uint32_t)((mt >> 1) & 1));
+      tc::tc_fence_after();
+      const int n_in = min(IPT, I - mt * IPT);    // inputs in this tile
+#pragma unroll 1
+      for (int sl = 0; sl < NP / SLICE_P; ++sl) {
+        const uint32_t tb = tmem + ((uint32_t)(qw * 32) << 16) + (uint32_t)(buf * N + sl * SLICE_P * C);
+#pragma unroll 1
+        for (int c8 = 0; c8 < SLICE_P * C; c8 += 8) {
+          float v[8];
+          tc::tmem_ld8(tb + c8, v);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) S[(c8 + q) * 128 + r] = v[q];
+        }
+        if (sl == NP / SLICE_P - 1) {             // accumulator fully read: release it early
+          tc::tc_fence_before();
+          tc::mbar_arrive(&acc_empty[buf]);
+        }
+        tc::named_bar_sync(1, 128);
+        for (int task = etid; task < SLICE_P * n_in; task += 128) {
+          const int pq = task % SLICE_P, il = task / SLICE_P;
+          const int64_t p = p0 + sl * SLICE_P + pq;
+          const int i = mt * IPT + il;
+          if (p >= P) continue;
+          float x, dx[NF > 0 ? NF : 1], ddx[NS > 0 ? NS : 1];
+          load_jet<NF, NS, false>(X, p, i, I, x, dx, ddx);
+          const int n0 = first_basis(x, bc);
+          float xb = 0.f, dxb[NF > 0 ? NF : 1], ddxb[NS > 0 ? NS : 1];
+#pragma unroll
+          for (int a = 0; a < NF; ++a) dxb[a] = 0.f;
+#pragma unroll
+          for (int a = 0; a < NS; ++a) ddxb[a] = 0.f;
+          const float* Sp = S + (pq * C) * 128 + il * bc.B;
+#pragma unroll
+          for (int rr = 0; rr < KMAX; ++rr) {
+            if (rr > bc.k) break;
+            const int n = n0 + rr;
+            if (n < 0 || n >= bc.B) continue;
+            float v0, v1, v2, v3;
+            hr_eval<M, (NS > 0 ? 3 : 2)>(basis_q(x, n, bc), bc.sc, v0, v1, v2, v3);
+            float ab[C];
+#pragma unroll
+            for (int c = 0; c < C; ++c) ab[c] = Sp[c * 128 + n];
+            xb = fmaf(ab[0], v1, xb);
+#pragma unroll
+            for (int a = 0; a < NF; ++a) {
+              xb = fmaf(ab[1 + a] * v2, dx[a], xb);
+              dxb[a] = fmaf(ab[1 + a], v1, dxb[a]);
+            }
+#pragma unroll
+            for (int a = 0; a < NS; ++a) {
+              const float g = ab[1 + NF + a];
+              xb = fmaf(g, fmaf(v3 * dx[a], dx[a], v2 * ddx[a]), xb);
+              dxb[a] = fmaf(2.f * g * v2, dx[a], dxb[a]);
+              ddxb[a] = fmaf(g, v1, ddxb[a]);
+            }
+          }
+          float* out = Xbar + p * (int64_t)(C * I) + i;
+          out[0] = xb;
+#pragma unroll
+          for (int a = 0; a < NF; ++a) out[(1 + a) * I] = dxb[a];
+#pragma unroll
+          for (int a = 0; a < NS; ++a) out[(1 + NF + a) * I] = ddxb[a];
+        }
+        tc::named_bar_sync(1, 128);
+      }
+    }
+  } else if (warp == DGR_MMA_WARP) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = tc::idesc_tf32(128, N);
+      for (int mt = 0; mt < nmt; ++mt) {
+        const int buf = mt & 1;
+        if (mt >= 2) {
+          tc::mbar_wait(&acc_empty[buf], (uint32_t)(((mt >> 1) - 1) & 1));
+          tc::tc_fence_after();
+        }
+        for (int kb = 0; kb < NKB; ++kb) {
+          const int g = mt * NKB + kb, s = g % NSTAGE;
+          tc::mbar_wait(&full_bar[s], (g / NSTAGE) & 1);
+          tc::tc_fence_after();
+          const float* w_hi = smem + s * (Cfg::W_STAGE_FLOATS + Cfg::Y_STAGE_FLOATS);
+          const float* w_lo = w_hi + 128 * TC_KB;
+          const float* y_hi = w_hi + Cfg::W_STAGE_FLOATS;
+          const float* y_lo = y_hi + N * TC_KB;
+#pragma unroll
+          for (int ks = 0; ks < TC_KB / 8; ++ks) {
+            const uint64_t wh = tc::smem_desc(tc::smem_u32(w_hi) + 2 * ks * 128 * 16, 128 * 16, 128);
+            const uint64_t wl = tc::smem_desc(tc::smem_u32(w_lo) + 2 * ks * 128 * 16, 128 * 16, 128);
+            const uint64_t yh = tc::smem_desc(tc::smem_u32(y_hi) + 2 * ks * N * 16, N * 16, 128);
+            const uint64_t yl = tc::smem_desc(tc::smem_u32(y_lo) + 2 * ks * N * 16, N * 16, 128);
+            const uint32_t d = tmem + (uint32_t)(buf * N);
+            tc::mma_tf32(d, wl, yh, idesc, (kb > 0 || ks > 0) ? 1u : 0u);
+            tc::mma_tf32(d, wh, yl, idesc, 1u);
+            tc::mma_tf32(d, wh, yh, idesc, 1u);
+          }
+          tc::mma_commit(&empty_bar[s]);
+        }
+        tc::mma_commit(&acc_full[buf]);
+      }
+    }
+    __syncwarp();
+  } else {
+    // ===================== bulk-copy producer of the pre-tiled W^T hi/lo stage
+    if (lane == 0) {
+      for (int g = 0; g < nblk; ++g) {
+        const int s = g % NSTAGE;
+        tc::mbar_wait(&empty_bar[s], ((g / NSTAGE) & 1) ^ 1);
+        tc::mbar_arrive_expect_tx(&full_bar[s], Cfg::W_STAGE_FLOATS * 4);
+        tc::bulk_g2s(smem + s * (Cfg::W_STAGE_FLOATS + Cfg::Y_STAGE_FLOATS), Wtiled + (int64_t)g * Cfg::W_STAGE_FLOATS,
+                     Cfg::W_STAGE_FLOATS * 4, &full_bar[s]);
+      }
+    }
+    __syncwarp();
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == DGR_MMA_WARP) tc::tmem_dealloc<Cfg::TMEM_COLS>(tmem);
+}
+
+}  // namespace

@@ -307,6 +307,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   if (warp == TC_MMA_WARP) tc::tmem_dealloc<Cfg::TMEM_COLS>(tmem);
 }
 
+}  // namespace
+
+#include "tc_dgrad.cuh"
+#include "tc_wgrad.cuh"
+
+namespace {
+
 // ---------------------------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------------------------
@@ -334,9 +341,19 @@ hrkan_status tc_refresh_weights(hrkan_net* net, cudaStream_t st) {
       if (cudaMalloc(&ls.w_fwd, n * sizeof(float)) != cudaSuccess) return fail(HRKAN_ENOMEM, "tc weight alloc");
     }
     const int64_t tot = (int64_t)ls.nkb * O * TC_KB;
-    const int pi_ = prof_pre(net, st);
-    k_tile_w_fwd<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(net->params + net->w_off[l], ls.w_fwd, O, K, ls.nkb);
-    HR_TRY(check_launch(net, "k_tile_w_fwd", HRKAN_K_OTHER, st, pi_));
+    HR_LAUNCH(HRKAN_K_OTHER, "k_tile_w_fwd",
+              k_tile_w_fwd<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(net->params + net->w_off[l], ls.w_fwd, O, K, ls.nkb));
+    // W^T tiles for the dgrad kernel (input-aligned M-tiles)
+    const int IPT = 128 / net->B;
+    ls.ntile_dgr = (I + IPT - 1) / IPT;
+    const size_t nd = (size_t)ls.ntile_dgr * (O / TC_KB) * 2 * 128 * TC_KB;
+    if (!ls.w_dgr) {
+      if (cudaMalloc(&ls.w_dgr, nd * sizeof(float)) != cudaSuccess) return fail(HRKAN_ENOMEM, "tc weight alloc");
+    }
+    const int64_t totd = (int64_t)ls.ntile_dgr * (O / TC_KB) * 128 * TC_KB;
+    HR_LAUNCH(HRKAN_K_OTHER, "k_tile_w_dgr",
+              k_tile_w_dgr<<<(unsigned)((totd + 255) / 256), 256, 0, st>>>(net->params + net->w_off[l], ls.w_dgr, O, I,
+                                                                          net->B, IPT, ls.ntile_dgr));
   }
   return HRKAN_OK;
 }
@@ -375,17 +392,86 @@ hrkan_status tc_forward_layer(hrkan_net* net, int l, const float* X, float* Y, i
   }
 }
 
-template <int NF, int NS, int M>
-hrkan_status tc_wgrad_layer(hrkan_net*, int, const float*, const float*, float*, float*, int64_t, cudaStream_t,
-                            bool* done) {
-  *done = false;
+template <int NF, int NS, int M, int OT>
+hrkan_status launch_wgrad_tc(hrkan_net* net, int l, const float* X, const float* Ybar, float* dW, float* db,
+                             int64_t n, cudaStream_t st) {
+  using Cfg = WgrCfg<NF, NS, M, OT>;
+  constexpr int C = Cfg::C, O = Cfg::O;
+  auto kfn = k_wgrad_tc<NF, NS, M, OT>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    HR_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
+    attr_set = true;
+  }
+  const int I = net->widths[l];
+  const int64_t K = (int64_t)I * net->B;
+  const int nmt = (int)((K + 127) / 128);
+  int nslab = (int)std::max<int64_t>(1, (4 * net->num_sms + nmt / 2) / nmt);
+  nslab = (int)std::min<int64_t>(nslab, std::max<int64_t>(1, n / 64));
+  int64_t slab = (n + nslab - 1) / nslab;
+  slab = (slab + 7) / 8 * 8;
+  nslab = (int)((n + slab - 1) / slab);
+  const size_t part_bytes = sizeof(float) * ((size_t)nslab * O * K + (size_t)64 * O);
+  HR_CUDA(net->tc_ws.ensure(part_bytes));
+  float* part = net->tc_ws.f();
+  float* part_b = part + (size_t)nslab * O * K;
+  HR_LAUNCH(HRKAN_K_WGRAD_HIDDEN, "k_wgrad_tc",
+            kfn<<<(unsigned)(nslab * nmt), WGR_THREADS, Cfg::SMEM_BYTES, st>>>(X, Ybar, part, n, I, nmt, slab,
+                                                                               net->tc_wseg, net->bc));
+  HR_LAUNCH(HRKAN_K_REDUCE, "k_reduce_slabs",
+            k_reduce_slabs<<<(unsigned)((O * K + 255) / 256), 256, 0, st>>>(part, nslab, (int64_t)O * K, dW));
+  const int nz = (int)std::min<int64_t>(64, std::max<int64_t>(1, n / 256));
+  HR_LAUNCH(HRKAN_K_REDUCE, "k_bias_part",
+            k_bias_part<<<dim3((O + 127) / 128, nz), 128, 0, st>>>(Ybar, C, O, n, part_b));
+  HR_LAUNCH(HRKAN_K_REDUCE, "k_reduce_bias", k_reduce_bias<<<(O + 127) / 128, 128, 0, st>>>(part_b, nz, O, db));
   return HRKAN_OK;
 }
 
 template <int NF, int NS, int M>
-hrkan_status tc_dgrad_layer(hrkan_net*, int, const float*, const float*, float*, int64_t, cudaStream_t, bool* done) {
+hrkan_status tc_wgrad_layer(hrkan_net* net, int l, const float* X, const float* Ybar, float* dW, float* db, int64_t n,
+                            cudaStream_t st, bool* done) {
   *done = false;
+  if (!tc_layer_ok(net, l) || n < 8) return HRKAN_OK;
+  const int O = net->widths[l + 1];
+  if (O == 128) HR_TRY(launch_wgrad_tc<NF, NS, M, 1>(net, l, X, Ybar, dW, db, n, st));
+  else HR_TRY(launch_wgrad_tc<NF, NS, M, 2>(net, l, X, Ybar, dW, db, n, st));
+  *done = true;
   return HRKAN_OK;
+}
+
+template <int NF, int NS, int M, int OT>
+hrkan_status launch_dgrad_tc(hrkan_net* net, int l, const float* X, const float* Ybar, float* Xbar, int64_t n,
+                             cudaStream_t st) {
+  using Cfg = DgrCfg<NF, NS, M, OT>;
+  auto kfn = k_dgrad_tc<NF, NS, M, OT>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    HR_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
+    attr_set = true;
+  }
+  const TcLayerState& ls = net->tc_layers[l];
+  const unsigned grid = (unsigned)((n + Cfg::NP - 1) / Cfg::NP);
+  HR_LAUNCH(HRKAN_K_DGRAD_HIDDEN, "k_dgrad_tc",
+            kfn<<<grid, DGR_THREADS, Cfg::SMEM_BYTES, st>>>(X, Ybar, ls.w_dgr, Xbar, n, net->widths[l], 128 / net->B,
+                                                            ls.ntile_dgr, net->bc));
+  return HRKAN_OK;
+}
+
+template <int NF, int NS, int M>
+hrkan_status tc_dgrad_layer(hrkan_net* net, int l, const float* X, const float* Ybar, float* Xbar, int64_t n,
+                            cudaStream_t st, bool* done) {
+  *done = false;
+  constexpr int C = 1 + NF + NS;
+  if constexpr (tc_np(C) == 0) {
+    return HRKAN_OK;
+  } else {
+    if (!tc_layer_ok(net, l) || l >= (int)net->tc_layers.size() || !net->tc_layers[l].w_dgr) return HRKAN_OK;
+    const int O = net->widths[l + 1];
+    if (O == 128) HR_TRY(launch_dgrad_tc<NF, NS, M, 1>(net, l, X, Ybar, Xbar, n, st));
+    else HR_TRY(launch_dgrad_tc<NF, NS, M, 2>(net, l, X, Ybar, Xbar, n, st));
+    *done = true;
+    return HRKAN_OK;
+  }
 }
 
 void tc_free(hrkan_net* net) {
