@@ -8,7 +8,8 @@
 //   d3v/dq3   =  4m(m-1) q t^{m-3} [3 - (2m-1) q^2]     (m = 2:  24 q)
 //   d^d v/dx^d = (2/w)^d d^d v/dq^d.
 // Strict interior (t > 0) only; every derivative is exactly 0 elsewhere (DESIGN.md reading:
-// ReLU(0) = 0, one-sided limits are not taken at the knots).
+// ReLU(0) = 0, one-sided limits are not taken at the knots).  A NaN input yields NaN values so that
+// non-finite inputs reach the loss and its non-finite flag.
 //
 // Supports ("same support as the B-splines"; reading 1):
 // s_n = lo + (n-k)h, e_n = s_n + (k+1)h, h = (hi-lo)/G, n = 0..G+k-1, so at any x the only
@@ -44,7 +45,10 @@ template <int M, int ND>
 __device__ __forceinline__ void hr_eval(float q, float sc, float& v0, float& v1, float& v2, float& v3) {
   const float q2 = q * q;
   const float t = 1.f - q2;
-  if (!(t > 0.f)) { v0 = v1 = v2 = v3 = 0.f; return; }
+  if (!(t > 0.f)) {                      // outside the support (or NaN: propagate it)
+    v0 = v1 = v2 = v3 = (t != t) ? t : 0.f;
+    return;
+  }
   // t^{m-3} ... t^m by repeated products (M is a compile-time constant)
   const float tm2 = ipow<(M >= 2 ? M - 2 : 0)>(t);
   const float tm1 = tm2 * t;

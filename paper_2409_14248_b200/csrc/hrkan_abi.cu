@@ -1,26 +1,15 @@
-// hrkan_abi.cu -- libhrkan.so: the C ABI of include/hrkan.h, the network object, the chunked
-// scheduler of the loss+gradient step and the host->device staging of host buffers.
+// hrkan_abi.cu -- libhrkan.so: the C ABI of include/hrkan.h, the network object and the host->device
+// staging of host buffers.  The chunked loss+gradient scheduler lives in pass_impl.cuh (one
+// translation unit per HR order m, pass_m<m>.cu).
 //
-// Every arithmetic step of the hot path runs in the kernels of simt_kernels.cuh / tc_kernels.cuh;
-// this file only validates arguments, owns device memory and sequences launches on the caller's
-// stream (SURVEY §3 "New build" call stack).
-#include <cuda_runtime.h>
-
-#include <algorithm>
-#include <cmath>
-#include <cstdint>
-#include <cstdio>
-#include <cstring>
-#include <string>
-#include <type_traits>
-#include <vector>
-
-#include "../../include/hrkan.h"
+// Every arithmetic step of the hot path runs in the kernels of simt_kernels.cuh, last_kernels.cuh
+// and tc_*.cuh; this file only validates arguments, owns device memory and sequences launches on
+// the caller's stream (SURVEY §3 "New build" call stack).
+#include "hrkan_internal.cuh"
 #include "simt_kernels.cuh"
+#include "tc_kernels.cuh"   // weight tiling for the tensor-core engine (tc_refresh_weights, tc_free)
 
-using namespace hrkan;
-
-namespace {
+namespace hrkan {
 
 thread_local std::string g_err;
 
@@ -28,177 +17,11 @@ hrkan_status fail(hrkan_status s, const std::string& msg) {
   g_err = msg;
   return s;
 }
+void clear_error() { g_err.clear(); }
 
-#define HR_CUDA(call)                                                                         \
-  do {                                                                                        \
-    cudaError_t e_ = (call);                                                                  \
-    if (e_ != cudaSuccess)                                                                    \
-      return fail(HRKAN_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_));          \
-  } while (0)
-
-#define HR_TRY(...)                     \
-  do {                                  \
-    hrkan_status s_ = (__VA_ARGS__);    \
-    if (s_ != HRKAN_OK) return s_;      \
-  } while (0)
-
-template <int V>
-using IC = std::integral_constant<int, V>;
-
-// RAII current-device switch (the caller's current device is restored).
-struct DeviceGuard {
-  int prev = -1;
-  explicit DeviceGuard(int dev) {
-    cudaGetDevice(&prev);
-    if (prev != dev) cudaSetDevice(dev);
-  }
-  ~DeviceGuard() {
-    int cur = -1;
-    cudaGetDevice(&cur);
-    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
-  }
-};
-
-bool is_device_ptr(const void* p) {
-  if (!p) return true;
-  cudaPointerAttributes a;
-  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
-    cudaGetLastError();
-    return false;
-  }
-  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
-}
-
-struct DevBuf {
-  void* p = nullptr;
-  size_t bytes = 0;
-  cudaError_t ensure(size_t n) {
-    if (n <= bytes) return cudaSuccess;
-    if (p) cudaFree(p);
-    p = nullptr;
-    bytes = 0;
-    cudaError_t e = cudaMalloc(&p, n);
-    if (e == cudaSuccess) bytes = n;
-    return e;
-  }
-  void release() {
-    if (p) cudaFree(p);
-    p = nullptr;
-    bytes = 0;
-  }
-  float* f() const { return static_cast<float*>(p); }
-};
-
-// Per-layer state of the tensor-core engine (tc_kernels.cuh).
-struct TcLayerState {
-  float* w_fwd = nullptr;   // pre-tiled, pre-split W for the forward kernel
-  float* w_dgr = nullptr;   // pre-tiled, pre-split W^T for the dgrad kernel
-  int nkb = 0;              // forward K-blocks
-  int ntile_dgr = 0;        // dgrad M-tiles
-};
-
-}  // namespace
-
-struct hrkan_net {
-  int device = 0;
-  int L = 0, D = 0, G = 0, k = 0, m = 0, B = 0;
-  float lo = -1.f, hi = 1.f;
-  std::vector<int> widths;
-  std::vector<int64_t> w_off, b_off;   // offsets into the flat parameter vector
-  int64_t n_params = 0;
-  int64_t max_layer_w = 0;
-  int max_width = 0;                   // max over widths[1..L]
-  BasisCfg bc{};
-  float* params = nullptr;             // flat, owned
-  float* adam_m = nullptr;
-  float* adam_v = nullptr;
-  int64_t adam_t = 0;
-  std::vector<float*> wt;              // derived: W_l transposed to [I][B][O]
-  bool derived_dirty = true;
-  int64_t chunk = 0;                   // 0 = auto
-  int engine = 0;
-  int64_t launches = 0;
-  int num_sms = 148;
-  // workspace
-  DevBuf jets, adj_a, adj_b, loss_part, w_part, b_part;
-  DevBuf st_int, st_f, st_bnd, st_gb, st_ini, st_gi, st_out, st_pts, st_u, st_du, st_d2u;
-  DevBuf tc_ws;                         // tensor-core path scratch
-  std::vector<TcLayerState> tc_layers;
-  int tc_seg = 32;                      // K-blocks per TMEM accumulation segment (precision bound)
-  int tc_wseg = 256;                    // wgrad stages per TMEM drain into the fp32 master
-  // device-time profiling (hrkan_profile_enable / hrkan_profile_read)
-  struct ProfEv { cudaEvent_t a, b; int cls; };
-  bool prof_on = false;
-  std::vector<ProfEv> prof_pool;
-  size_t prof_used = 0;
-};
+}  // namespace hrkan
 
 namespace {
-
-constexpr int NZ_MAX = 64;
-
-int prof_pre(hrkan_net* net, cudaStream_t st) {
-  if (!net->prof_on) return -1;
-  if (net->prof_used == net->prof_pool.size()) {
-    hrkan_net::ProfEv ev{};
-    if (cudaEventCreate(&ev.a) != cudaSuccess || cudaEventCreate(&ev.b) != cudaSuccess) return -1;
-    net->prof_pool.push_back(ev);
-  }
-  cudaEventRecord(net->prof_pool[net->prof_used].a, st);
-  return (int)net->prof_used++;
-}
-
-hrkan_status check_launch(hrkan_net* net, const char* what, int cls = HRKAN_K_OTHER, cudaStream_t st = nullptr,
-                          int prof_idx = -1) {
-  net->launches++;
-  cudaError_t e = cudaGetLastError();
-  if (prof_idx >= 0) {
-    cudaEventRecord(net->prof_pool[prof_idx].b, st);
-    net->prof_pool[prof_idx].cls = cls;
-  }
-  if (e != cudaSuccess) return fail(HRKAN_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
-  return HRKAN_OK;
-}
-
-// Launch statement bracketed by profiling events and followed by the launch-error check.
-#define HR_LAUNCH(CLS, NAME, ...)                                   \
-  do {                                                              \
-    const int pi_ = prof_pre(net, st);                              \
-    __VA_ARGS__;                                                    \
-    HR_TRY(check_launch(net, NAME, CLS, st, pi_));                  \
-  } while (0)
-
-}  // namespace
-
-#include "tc_kernels.cuh"   // tensor-core (tcgen05) hidden-layer engine; needs hrkan_net + helpers
-
-namespace {
-
-int64_t auto_chunk(const hrkan_net* net) {
-  if (net->chunk > 0) return net->chunk;
-  const int C = 1 + 2 * net->D;
-  int64_t sumw = 0;
-  for (int l = 1; l <= net->L; ++l) sumw += net->widths[l];
-  const double bytes_per_point = 4.0 * C * (double)(sumw + 2 * net->max_width) * 1.0;
-  const double budget = 12.0e9;
-  int64_t c = (int64_t)(budget / bytes_per_point);
-  c = std::min<int64_t>(c, 1 << 20);
-  c = std::max<int64_t>(256, c / 256 * 256);
-  return c;
-}
-
-// Workspace for chunks of Pc points with C channels.
-hrkan_status ensure_workspace(hrkan_net* net, int64_t Pc, int C) {
-  int64_t sumw = 0;
-  for (int l = 1; l <= net->L; ++l) sumw += net->widths[l];
-  HR_CUDA(net->jets.ensure(sizeof(float) * (size_t)Pc * C * sumw));
-  HR_CUDA(net->adj_a.ensure(sizeof(float) * (size_t)Pc * C * net->max_width));
-  HR_CUDA(net->adj_b.ensure(sizeof(float) * (size_t)Pc * C * net->max_width));
-  HR_CUDA(net->loss_part.ensure(sizeof(float) * 2 * (size_t)((Pc + 255) / 256 + 1)));
-  HR_CUDA(net->w_part.ensure(sizeof(float) * (size_t)NZ_MAX * net->max_layer_w));
-  HR_CUDA(net->b_part.ensure(sizeof(float) * (size_t)NZ_MAX * net->max_width));
-  return HRKAN_OK;
-}
 
 hrkan_status refresh_derived(hrkan_net* net, cudaStream_t st) {
   if (!net->derived_dirty) return HRKAN_OK;
@@ -225,169 +48,18 @@ hrkan_status stage_in(const float* src, int64_t n, DevBuf& buf, cudaStream_t st,
   return HRKAN_OK;
 }
 
-template <class F>
-hrkan_status with_m(int m, F&& f) {
-  switch (m) {
-    case 2: return f(IC<2>{});
-    case 3: return f(IC<3>{});
-    case 4: return f(IC<4>{});
-    case 5: return f(IC<5>{});
-    case 6: return f(IC<6>{});
-    case 7: return f(IC<7>{});
-    case 8: return f(IC<8>{});
-  }
-  return fail(HRKAN_EINVAL, "m must be in [2, 8]");
-}
-
-enum PassKind { PASS_JET = 0, PASS_INTERIOR = 1, PASS_BOUNDARY = 2 };
-
-struct PassArgs {
-  PassKind kind;
-  const float* pts;        // [P][D] device
-  int64_t P;
-  const float* forcing;    // interior Poisson (device) or null
-  const float* g;          // boundary targets (device)
-  float* u; float* du; float* d2u;   // PASS_JET outputs (device)
-  float* grad;             // flat gradient (device)
-  float* out_loss;         // device scalar slot
-  float* out_flag;
-  const hrkan_pde* pde;
-  float inv_n;             // 1/N_int_global or 1/N_bi_global
-};
-
-// Forward + (optional) loss/seeds + reverse over one point set, chunk by chunk.
-template <int NF, int NS, int M>
-hrkan_status run_pass(hrkan_net* net, const PassArgs& a, cudaStream_t st) {
-  constexpr int C = 1 + NF + NS;
-  const int L = net->L, D = net->D;
-  const int64_t Pc = std::min<int64_t>(auto_chunk(net), std::max<int64_t>(a.P, 1));
-  HR_TRY(ensure_workspace(net, Pc, C));
-  // layer-input jet buffers: jet[l] for l = 1..L (jet[L] = network output [P][C][1])
-  std::vector<float*> jet(L + 1, nullptr);
-  {
-    float* q = net->jets.f();
-    for (int l = 1; l <= L; ++l) {
-      jet[l] = q;
-      q += (size_t)Pc * C * net->widths[l];
-    }
-  }
-  const BasisCfg bc = net->bc;
-  for (int64_t c0 = 0; c0 < a.P; c0 += Pc) {
-    const int64_t n = std::min(Pc, a.P - c0);
-    const float* X0 = a.pts + c0 * D;
-    // ---------------- forward (SURVEY §8(a) a1, a2, a3/a8 value part)
-    for (int l = 0; l < L; ++l) {
-      const int I = net->widths[l], O = net->widths[l + 1];
-      const float* in = (l == 0) ? X0 : jet[l];
-      bool done = false;
-      if (l > 0) HR_TRY(tc_forward_layer<NF, NS, M>(net, l, in, jet[l + 1], n, st, &done));
-      if (!done) {
-        const int64_t tot = n * O;
-        const unsigned grid = (unsigned)((tot + 255) / 256);
-        const int cls = (l == 0) ? HRKAN_K_FWD_FIRST : (l == L - 1 ? HRKAN_K_FWD_LAST : HRKAN_K_FWD_HIDDEN);
-        if (l == 0)
-          HR_LAUNCH(cls, "k_fwd_simt", k_fwd_simt<NF, NS, M, true><<<grid, 256, 0, st>>>(in, net->wt[l], net->params + net->b_off[l], jet[l + 1], n, I, O, bc));
-        else
-          HR_LAUNCH(cls, "k_fwd_simt", k_fwd_simt<NF, NS, M, false><<<grid, 256, 0, st>>>(in, net->wt[l], net->params + net->b_off[l], jet[l + 1], n, I, O, bc));
-      }
-    }
-    if (a.kind == PASS_JET) {
-      if constexpr (NF == NS && NF >= 1) {
-        HR_LAUNCH(HRKAN_K_OTHER, "k_scatter_jet",
-                  k_scatter_jet<NF><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(jet[L], n, a.u ? a.u + c0 : nullptr,
-                                                                                  a.du ? a.du + c0 * NF : nullptr,
-                                                                                  a.d2u ? a.d2u + c0 * NF : nullptr));
-      }
-      continue;
-    }
-    // ---------------- residual, loss partials, seeds (a3 / a8)
-    const unsigned nb = (unsigned)((n + 255) / 256);
-    float* ybar = net->adj_a.f();
-    float* xbar = net->adj_b.f();
-    float* part = net->loss_part.f();
-    if (a.kind == PASS_INTERIOR) {
-      const hrkan_pde& pde = *a.pde;
-      const float* f = a.forcing ? a.forcing + c0 : nullptr;
-      if (pde.kind == HRKAN_BURGERS) {
-        if constexpr (NF == 2 && NS == 1)
-          HR_LAUNCH(HRKAN_K_LOSS, "k_interior_loss",
-                    k_interior_loss<2, 2, 1, true><<<nb, 256, 0, st>>>(jet[L], X0, f, ybar, part, n, pde.alpha, pde.adv, pde.visc, a.inv_n));
-        else
-          return fail(HRKAN_EINVAL, "internal: Burgers pass needs NF=2, NS=1");
-      } else {
-        if constexpr (NF == NS && NF >= 1)
-          HR_LAUNCH(HRKAN_K_LOSS, "k_interior_loss",
-                    k_interior_loss<NF, NF, NS, false><<<nb, 256, 0, st>>>(jet[L], X0, f, ybar, part, n, pde.alpha, 0.f, 0.f, a.inv_n));
-        else
-          return fail(HRKAN_EINVAL, "internal: Poisson pass needs NF=NS=D");
-      }
-      HR_LAUNCH(HRKAN_K_LOSS, "k_finish_loss",
-                k_finish_loss<<<1, 256, 0, st>>>(part, (int)nb, pde.alpha * a.inv_n, a.out_loss, a.out_flag));
-    } else {
-      HR_LAUNCH(HRKAN_K_LOSS, "k_boundary_loss", k_boundary_loss<<<nb, 256, 0, st>>>(jet[L], a.g + c0, ybar, part, n, a.inv_n));
-      HR_LAUNCH(HRKAN_K_LOSS, "k_finish_loss", k_finish_loss<<<1, 256, 0, st>>>(part, (int)nb, a.inv_n, a.out_loss, a.out_flag));
-    }
-    // ---------------- reverse (a4-a7)
-    for (int l = L - 1; l >= 0; --l) {
-      const int I = net->widths[l], O = net->widths[l + 1];
-      const float* in = (l == 0) ? X0 : jet[l];
-      float* dW = a.grad + net->w_off[l];
-      float* db = a.grad + net->b_off[l];
-      bool done = false;
-      if (l > 0 && l < L - 1) HR_TRY(tc_wgrad_layer<NF, NS, M>(net, l, in, ybar, dW, db, n, st, &done));
-      if (!done) {
-        const dim3 blk(WG_J, WG_I);
-        const int gx = (O + WG_J - 1) / WG_J, gy = (I + WG_I - 1) / WG_I;
-        int nz = (int)std::max<int64_t>(1, (4 * net->num_sms + gx * gy - 1) / (gx * gy));
-        nz = (int)std::min<int64_t>(nz, std::max<int64_t>(1, n / 64));
-        nz = std::min(nz, NZ_MAX);
-        const dim3 grid(gx, gy, nz);
-        const size_t smem = sizeof(float) * WG_I * net->B * WG_J;
-        const int cls = (l == 0) ? HRKAN_K_WGRAD_FIRST : (l == L - 1 ? HRKAN_K_WGRAD_LAST : HRKAN_K_WGRAD_HIDDEN);
-        if (l == 0) {
-          auto kfn = k_wgrad_simt<NF, NS, M, true>;
-          if (smem > 48 * 1024) HR_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-          HR_LAUNCH(cls, "k_wgrad_simt", kfn<<<grid, blk, smem, st>>>(in, ybar, net->w_part.f(), net->b_part.f(), n, I, O, bc));
-        } else {
-          auto kfn = k_wgrad_simt<NF, NS, M, false>;
-          if (smem > 48 * 1024) HR_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-          HR_LAUNCH(cls, "k_wgrad_simt", kfn<<<grid, blk, smem, st>>>(in, ybar, net->w_part.f(), net->b_part.f(), n, I, O, bc));
-        }
-        const int64_t nW = (int64_t)O * I * net->B;
-        HR_LAUNCH(HRKAN_K_REDUCE, "k_reduce_parts",
-                  k_reduce_parts<<<(unsigned)((nW + O + 255) / 256), 256, 0, st>>>(net->w_part.f(), net->b_part.f(), nz, nW, O, dW, db));
-      }
-      if (l > 0) {
-        bool ddone = false;
-        if (l < L - 1) HR_TRY(tc_dgrad_layer<NF, NS, M>(net, l, in, ybar, xbar, n, st, &ddone));
-        if (!ddone) {
-          const int64_t tot = n * I;
-          HR_LAUNCH(l == L - 1 ? HRKAN_K_DGRAD_LAST : HRKAN_K_DGRAD_HIDDEN, "k_dgrad_simt",
-                    k_dgrad_simt<NF, NS, M><<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(in, net->params + net->w_off[l], ybar, xbar, n, I, O, bc));
-        }
-        std::swap(ybar, xbar);
-      }
-    }
-  }
-  return HRKAN_OK;
-}
-
-template <class F>
-hrkan_status with_channels(int nf, int ns, F&& f) {
-  if (nf == 0 && ns == 0) return f(IC<0>{}, IC<0>{});
-  if (nf == 1 && ns == 1) return f(IC<1>{}, IC<1>{});
-  if (nf == 2 && ns == 1) return f(IC<2>{}, IC<1>{});
-  if (nf == 2 && ns == 2) return f(IC<2>{}, IC<2>{});
-  if (nf == 3 && ns == 3) return f(IC<3>{}, IC<3>{});
-  return fail(HRKAN_EINVAL, "internal: unsupported channel set");
-}
 
 hrkan_status dispatch_pass(hrkan_net* net, int nf, int ns, const PassArgs& a, cudaStream_t st) {
-  return with_channels(nf, ns, [&](auto NFc, auto NSc) {
-    return with_m(net->m, [&](auto Mc) {
-      return run_pass<decltype(NFc)::value, decltype(NSc)::value, decltype(Mc)::value>(net, a, st);
-    });
-  });
+  switch (net->m) {
+    case 2: return dispatch_pass_m2(net, nf, ns, a, st);
+    case 3: return dispatch_pass_m3(net, nf, ns, a, st);
+    case 4: return dispatch_pass_m4(net, nf, ns, a, st);
+    case 5: return dispatch_pass_m5(net, nf, ns, a, st);
+    case 6: return dispatch_pass_m6(net, nf, ns, a, st);
+    case 7: return dispatch_pass_m7(net, nf, ns, a, st);
+    case 8: return dispatch_pass_m8(net, nf, ns, a, st);
+  }
+  return fail(HRKAN_EINVAL, "m must be in [2, 8]");
 }
 
 }  // namespace
@@ -397,11 +69,11 @@ hrkan_status dispatch_pass(hrkan_net* net, int nf, int ns, const PassArgs& a, cu
 // =============================================================================================
 extern "C" {
 
-const char* hrkan_last_error(void) { return g_err.c_str(); }
+const char* hrkan_last_error(void) { return hrkan::g_err.c_str(); }
 
 hrkan_status hrkan_create(const int32_t* widths, int32_t n_widths, int32_t G, int32_t k, int32_t m, float grid_lo,
                           float grid_hi, uint64_t seed, int32_t device, hrkan_net_t* out) {
-  g_err.clear();
+  clear_error();
   if (!out) return fail(HRKAN_EINVAL, "out is NULL");
   *out = nullptr;
   if (!widths || n_widths < 2) return fail(HRKAN_EINVAL, "need at least 2 widths");
@@ -540,7 +212,7 @@ hrkan_status hrkan_forward_jet(hrkan_net_t net, const float* pts, int64_t P, flo
   if (P < 0) return fail(HRKAN_EINVAL, "P must be >= 0");
   if (P == 0) return HRKAN_OK;
   if (!pts) return fail(HRKAN_EINVAL, "pts is NULL");
-  g_err.clear();
+  clear_error();
   DeviceGuard dg(net->device);
   cudaStream_t st = (cudaStream_t)stream;
   const int D = net->D;
@@ -582,7 +254,7 @@ hrkan_status hrkan_pinn_loss_grad(hrkan_net_t net, const hrkan_pde* pde, const f
   if (pde->kind != HRKAN_POISSON && pde->kind != HRKAN_BURGERS) return fail(HRKAN_EINVAL, "unknown pde kind");
   if (pde->kind == HRKAN_BURGERS && net->D != 2) return fail(HRKAN_EINVAL, "Burgers needs D = 2 (x, t)");
   if (!std::isfinite(pde->alpha)) return fail(HRKAN_EINVAL, "alpha must be finite");
-  g_err.clear();
+  clear_error();
   DeviceGuard dg(net->device);
   cudaStream_t st = (cudaStream_t)stream;
   const int D = net->D;
@@ -695,7 +367,7 @@ void hrkan_free(hrkan_net_t net) {
   cudaFree(net->adam_m);
   cudaFree(net->adam_v);
   for (float* p : net->wt) cudaFree(p);
-  DevBuf* bufs[] = {&net->jets, &net->adj_a, &net->adj_b, &net->loss_part, &net->w_part, &net->b_part,
+  DevBuf* bufs[] = {&net->jets, &net->adj_a, &net->adj_b, &net->loss_part, &net->w_part, &net->b_part, &net->last_part,
                     &net->st_int, &net->st_f, &net->st_bnd, &net->st_gb, &net->st_ini, &net->st_gi,
                     &net->st_out, &net->st_pts, &net->st_u, &net->st_du, &net->st_d2u, &net->tc_ws};
   for (DevBuf* b : bufs) b->release();

@@ -1,0 +1,228 @@
+// hrkan_internal.cuh -- the network object and the host helpers shared by the translation units of
+// libhrkan.so (hrkan_abi.cu: the C ABI; pass_m<M>.cu: the chunked loss+gradient scheduler
+// instantiated for HR order M, compiled in parallel).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <type_traits>
+#include <vector>
+
+#include "../../include/hrkan.h"
+#include "hr_basis.cuh"
+
+using namespace hrkan;
+
+namespace hrkan {
+
+// Records the thread-local error message returned by hrkan_last_error() (hrkan_abi.cu).
+hrkan_status fail(hrkan_status s, const std::string& msg);
+void clear_error();
+
+#define HR_CUDA(call)                                                                         \
+  do {                                                                                        \
+    cudaError_t e_ = (call);                                                                  \
+    if (e_ != cudaSuccess)                                                                    \
+      return fail(HRKAN_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_));          \
+  } while (0)
+
+#define HR_TRY(...)                     \
+  do {                                  \
+    hrkan_status s_ = (__VA_ARGS__);    \
+    if (s_ != HRKAN_OK) return s_;      \
+  } while (0)
+
+template <int V>
+using IC = std::integral_constant<int, V>;
+
+// RAII current-device switch (the caller's current device is restored).
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+inline bool is_device_ptr(const void* p) {
+  if (!p) return true;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  cudaError_t ensure(size_t n) {
+    if (n <= bytes) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    cudaError_t e = cudaMalloc(&p, n);
+    if (e == cudaSuccess) bytes = n;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  float* f() const { return static_cast<float*>(p); }
+};
+
+// Per-layer state of the tensor-core engine (tc_kernels.cuh).
+struct TcLayerState {
+  float* w_fwd = nullptr;   // pre-tiled, pre-split W for the forward kernel
+  float* w_dgr = nullptr;   // pre-tiled, pre-split W^T for the dgrad kernel
+  int nkb = 0;              // forward K-blocks
+  int ntile_dgr = 0;        // dgrad M-tiles
+};
+
+}  // namespace hrkan
+
+using namespace hrkan;
+
+struct hrkan_net {
+  int device = 0;
+  int L = 0, D = 0, G = 0, k = 0, m = 0, B = 0;
+  float lo = -1.f, hi = 1.f;
+  std::vector<int> widths;
+  std::vector<int64_t> w_off, b_off;   // offsets into the flat parameter vector
+  int64_t n_params = 0;
+  int64_t max_layer_w = 0;
+  int max_width = 0;                   // max over widths[1..L]
+  BasisCfg bc{};
+  float* params = nullptr;             // flat, owned
+  float* adam_m = nullptr;
+  float* adam_v = nullptr;
+  int64_t adam_t = 0;
+  std::vector<float*> wt;              // derived: W_l transposed to [I][B][O]
+  bool derived_dirty = true;
+  int64_t chunk = 0;                   // 0 = auto
+  int engine = 0;
+  int64_t launches = 0;
+  int num_sms = 148;
+  // workspace
+  DevBuf jets, adj_a, adj_b, loss_part, w_part, b_part, last_part;
+  DevBuf st_int, st_f, st_bnd, st_gb, st_ini, st_gi, st_out, st_pts, st_u, st_du, st_d2u;
+  DevBuf tc_ws;                         // tensor-core path scratch
+  std::vector<TcLayerState> tc_layers;
+  int tc_seg = 32;                      // K-blocks per TMEM accumulation segment (precision bound)
+  int tc_wseg = 256;                    // wgrad stages per TMEM drain into the fp32 master
+  // device-time profiling (hrkan_profile_enable / hrkan_profile_read)
+  struct ProfEv { cudaEvent_t a, b; int cls; };
+  bool prof_on = false;
+  std::vector<ProfEv> prof_pool;
+  size_t prof_used = 0;
+};
+
+namespace hrkan {
+
+constexpr int NZ_MAX = 64;
+
+inline int prof_pre(hrkan_net* net, cudaStream_t st) {
+  if (!net->prof_on) return -1;
+  if (net->prof_used == net->prof_pool.size()) {
+    hrkan_net::ProfEv ev{};
+    if (cudaEventCreate(&ev.a) != cudaSuccess || cudaEventCreate(&ev.b) != cudaSuccess) return -1;
+    net->prof_pool.push_back(ev);
+  }
+  cudaEventRecord(net->prof_pool[net->prof_used].a, st);
+  return (int)net->prof_used++;
+}
+
+inline hrkan_status check_launch(hrkan_net* net, const char* what, int cls = HRKAN_K_OTHER, cudaStream_t st = nullptr,
+                          int prof_idx = -1) {
+  net->launches++;
+  cudaError_t e = cudaGetLastError();
+  if (prof_idx >= 0) {
+    cudaEventRecord(net->prof_pool[prof_idx].b, st);
+    net->prof_pool[prof_idx].cls = cls;
+  }
+  if (e != cudaSuccess) return fail(HRKAN_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  return HRKAN_OK;
+}
+
+// Launch statement bracketed by profiling events and followed by the launch-error check.
+#define HR_LAUNCH(CLS, NAME, ...)                                   \
+  do {                                                              \
+    const int pi_ = prof_pre(net, st);                              \
+    __VA_ARGS__;                                                    \
+    HR_TRY(check_launch(net, NAME, CLS, st, pi_));                  \
+  } while (0)
+
+}  // namespace hrkan
+
+
+namespace hrkan {
+
+inline int64_t auto_chunk(const hrkan_net* net) {
+  if (net->chunk > 0) return net->chunk;
+  const int C = 1 + 2 * net->D;
+  int64_t sumw = 0;
+  for (int l = 1; l <= net->L; ++l) sumw += net->widths[l];
+  const double bytes_per_point = 4.0 * C * (double)(sumw + 2 * net->max_width) * 1.0;
+  const double budget = 12.0e9;
+  int64_t c = (int64_t)(budget / bytes_per_point);
+  c = std::min<int64_t>(c, 1 << 20);
+  c = std::max<int64_t>(256, c / 256 * 256);
+  return c;
+}
+
+// Workspace for chunks of Pc points with C channels.
+inline hrkan_status ensure_workspace(hrkan_net* net, int64_t Pc, int C) {
+  int64_t sumw = 0;
+  for (int l = 1; l <= net->L; ++l) sumw += net->widths[l];
+  HR_CUDA(net->jets.ensure(sizeof(float) * (size_t)Pc * C * sumw));
+  HR_CUDA(net->adj_a.ensure(sizeof(float) * (size_t)Pc * C * net->max_width));
+  HR_CUDA(net->adj_b.ensure(sizeof(float) * (size_t)Pc * C * net->max_width));
+  HR_CUDA(net->loss_part.ensure(sizeof(float) * 2 * (size_t)((Pc + 255) / 256 + 1)));
+  HR_CUDA(net->w_part.ensure(sizeof(float) * (size_t)NZ_MAX * net->max_layer_w));
+  HR_CUDA(net->b_part.ensure(sizeof(float) * (size_t)NZ_MAX * net->max_width));
+  return HRKAN_OK;
+}
+
+enum PassKind { PASS_JET = 0, PASS_INTERIOR = 1, PASS_BOUNDARY = 2 };
+
+struct PassArgs {
+  PassKind kind;
+  const float* pts;        // [P][D] device
+  int64_t P;
+  const float* forcing;    // interior Poisson (device) or null
+  const float* g;          // boundary targets (device)
+  float* u; float* du; float* d2u;   // PASS_JET outputs (device)
+  float* grad;             // flat gradient (device)
+  float* out_loss;         // device scalar slot
+  float* out_flag;
+  const hrkan_pde* pde;
+  float inv_n;             // 1/N_int_global or 1/N_bi_global
+};
+
+// Forward + (optional) loss/seeds + reverse over one point set, chunk by chunk.
+
+// One scheduler per HR order m (pass_m<m>.cu).
+#define HRKAN_DECLARE_DISPATCH(MM) \
+  hrkan_status dispatch_pass_m##MM(hrkan_net* net, int nf, int ns, const PassArgs& a, cudaStream_t st);
+HRKAN_DECLARE_DISPATCH(2)
+HRKAN_DECLARE_DISPATCH(3)
+HRKAN_DECLARE_DISPATCH(4)
+HRKAN_DECLARE_DISPATCH(5)
+HRKAN_DECLARE_DISPATCH(6)
+HRKAN_DECLARE_DISPATCH(7)
+HRKAN_DECLARE_DISPATCH(8)
+
+}  // namespace hrkan

@@ -1,0 +1,221 @@
+// last_kernels.cuh -- the output layer (O = 1) fused with the residual, the loss and its own reverse
+// pass, one warp per collocation point.
+//
+// The output layer contracts K = I(G+k) features into ONE neuron, so per point it is a reduction
+// over (i, n), not a GEMM: lanes own inputs i = lane, lane+32, ... (coalesced loads of the saved
+// jet X[p][c][i]), each visits only the k+1 bases that are non-zero at x_i (compact support,
+// PAPER.md:90-94), and a butterfly reduction gives every lane the output jet.  Then, without
+// leaving the kernel:
+//   residual   Poisson r = sum_a u_aa - f, f = -D pi^2 prod sin(pi xi_a) (Eq. 3) or forcing;
+//              Burgers r = u_t + adv u u_x - visc u_xx (Eq. 5); boundary e = u - g;
+//   seeds      ybar_c = dL/d(output jet channel c), L = alpha/N_int sum r^2 + 1/N_bi sum e^2;
+//   reverse    per (p, i), with w_n = W[0, i, n] and T_d = sum_n w_n v_n^(d)(x_i):
+//                dW[0,i,n] += y0 v_n + g1 v'_n + g2 v''_n,   g1 = sum_a y1_a dx_a + sum_a y2_a ddx_a,
+//                                                            g2 = sum_a y2_a dx_a^2
+//                xbar      = y0 T1 + g1 T2 + g2 T3
+//                dxbar_a   = y1_a T1 + 2 y2_a dx_a T2,        ddxbar_a = y2_a T1
+//              (the jet chain rule of SURVEY §8(c) c5 with Abar^c = ybar_c W specialised to O = 1).
+// dW is accumulated per warp in shared memory acc[warp][n][i] (lanes own distinct i: no atomics,
+// conflict-free), reduced over the block's warps in a fixed order into part[block][I*B + 4]
+// (+ db, sum r^2, non-finite count), and k_reduce_last sums the blocks in a fixed order: the
+// result is bitwise reproducible for a fixed grid.
+#pragma once
+
+namespace {   // internal linkage: every translation unit owns its kernels
+using namespace hrkan;
+
+constexpr int LF_WARPS = 4;
+enum LastMode { LAST_JET = 0, LAST_POISSON = 1, LAST_BURGERS = 2, LAST_BOUNDARY = 3 };
+
+template <int NF, int NS, int M, int MODE, bool FIRST>
+__global__ void __launch_bounds__(32 * LF_WARPS)
+    k_last_fused(const float* __restrict__ X, const float* __restrict__ W, const float* __restrict__ bias,
+                 int64_t P, int I, BasisCfg bc,
+                 float* __restrict__ u_out, float* __restrict__ du_out, float* __restrict__ d2u_out,
+                 const float* __restrict__ pts, const float* __restrict__ forcing, const float* __restrict__ gtar,
+                 float alpha, float adv, float visc, float inv_n,
+                 float* __restrict__ Xbar, float* __restrict__ part) {
+  constexpr int C = 1 + NF + NS;
+  constexpr int D = (MODE == LAST_POISSON || MODE == LAST_JET) ? NF : 2;
+  extern __shared__ float acc_sh[];     // [LF_WARPS][B][I]   (not used by LAST_JET)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int B = bc.B;
+  const int IB = I * B;
+  float* acc = acc_sh + (size_t)warp * IB;
+  if (MODE != LAST_JET) {
+    for (int t = lane; t < IB; t += 32) acc[t] = 0.f;
+    __syncwarp();
+  }
+  const int64_t lo = (P * blockIdx.x) / gridDim.x, hi = (P * (blockIdx.x + 1)) / gridDim.x;
+  const float b0 = __ldg(bias);
+  float db = 0.f, sq = 0.f, bad = 0.f;
+  for (int64_t p = lo + warp; p < hi; p += LF_WARPS) {
+    // ---------------- pass 1: output jet
+    float s[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) s[c] = 0.f;
+    for (int i = lane; i < I; i += 32) {
+      float x, dx[NF > 0 ? NF : 1], ddx[NS > 0 ? NS : 1];
+      load_jet<NF, NS, FIRST>(X, p, i, I, x, dx, ddx);
+      if (x != x) s[0] += x;            // propagate NaN inputs into the residual / flag
+      const int n0 = first_basis(x, bc);
+      float T0 = 0.f, T1 = 0.f, T2 = 0.f;
+#pragma unroll
+      for (int r = 0; r < KMAX; ++r) {
+        if (r > bc.k) break;
+        const int n = n0 + r;
+        if (n < 0 || n >= B) continue;
+        float v0, v1, v2, v3;
+        hr_eval<M, (NS > 0 ? 2 : (NF > 0 ? 1 : 0))>(basis_q(x, n, bc), bc.sc, v0, v1, v2, v3);
+        const float w = __ldg(W + i * B + n);
+        T0 = fmaf(w, v0, T0);
+        T1 = fmaf(w, v1, T1);
+        T2 = fmaf(w, v2, T2);
+      }
+      s[0] += T0;
+#pragma unroll
+      for (int a = 0; a < NF; ++a) s[1 + a] = fmaf(T1, dx[a], s[1 + a]);
+#pragma unroll
+      for (int a = 0; a < NS; ++a) s[1 + NF + a] = fmaf(T2 * dx[a], dx[a], fmaf(T1, ddx[a], s[1 + NF + a]));
+    }
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s[c] += __shfl_xor_sync(0xffffffffu, s[c], o);
+    }
+    s[0] += b0;
+    if (MODE == LAST_JET) {
+      if (lane == 0) {
+        if (u_out) u_out[p] = s[0];
+#pragma unroll
+        for (int a = 0; a < NF; ++a) {
+          if (du_out) du_out[p * NF + a] = s[1 + a];
+          if (d2u_out) d2u_out[p * NF + a] = s[1 + NF + a];
+        }
+      }
+      continue;
+    }
+    // ---------------- residual, loss, seeds (identical in every lane)
+    float y[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) y[c] = 0.f;
+    float r;
+    if (MODE == LAST_BOUNDARY) {
+      r = s[0] - __ldg(gtar + p);
+      y[0] = 2.f * r * inv_n;
+    } else if (MODE == LAST_BURGERS) {
+      r = s[2] + adv * s[0] * s[1] - visc * s[1 + NF];
+      const float g = 2.f * alpha * r * inv_n;
+      y[0] = g * adv * s[1];
+      y[1] = g * adv * s[0];
+      y[2] = g;
+      y[1 + NF] = -g * visc;
+    } else {
+      float f;
+      if (forcing) {
+        f = __ldg(forcing + p);
+      } else {
+        float prod = 1.f;
+#pragma unroll
+        for (int a = 0; a < D; ++a) prod *= sinpif(__ldg(pts + p * D + a));
+        f = -(float)D * 9.8696044010893586f * prod;   // -D pi^2 prod_a sin(pi xi_a)
+      }
+      float lap = 0.f;
+#pragma unroll
+      for (int a = 0; a < NS; ++a) lap += s[1 + NF + a];
+      r = lap - f;
+      const float g = 2.f * alpha * r * inv_n;
+#pragma unroll
+      for (int a = 0; a < NS; ++a) y[1 + NF + a] = g;
+    }
+    sq = fmaf(r, r, sq);
+    bad += isfinite(r) ? 0.f : 1.f;
+    db += y[0];
+    // ---------------- pass 2: dW and the adjoint of the input jet
+    for (int i = lane; i < I; i += 32) {
+      float x, dx[NF > 0 ? NF : 1], ddx[NS > 0 ? NS : 1];
+      load_jet<NF, NS, FIRST>(X, p, i, I, x, dx, ddx);
+      float g1 = 0.f, g2 = 0.f;
+#pragma unroll
+      for (int a = 0; a < NF; ++a) g1 = fmaf(y[1 + a], dx[a], g1);
+#pragma unroll
+      for (int a = 0; a < NS; ++a) {
+        g1 = fmaf(y[1 + NF + a], ddx[a], g1);
+        g2 = fmaf(y[1 + NF + a] * dx[a], dx[a], g2);
+      }
+      const int n0 = first_basis(x, bc);
+      float T1 = 0.f, T2 = 0.f, T3 = 0.f;
+#pragma unroll
+      for (int rr = 0; rr < KMAX; ++rr) {
+        if (rr > bc.k) break;
+        const int n = n0 + rr;
+        if (n < 0 || n >= B) continue;
+        float v0, v1, v2, v3;
+        hr_eval<M, (NS > 0 ? 3 : (NF > 0 ? 2 : 1))>(basis_q(x, n, bc), bc.sc, v0, v1, v2, v3);
+        acc[n * I + i] += fmaf(y[0], v0, fmaf(g1, v1, g2 * v2));
+        if (!FIRST) {
+          const float w = __ldg(W + i * B + n);
+          T1 = fmaf(w, v1, T1);
+          T2 = fmaf(w, v2, T2);
+          T3 = fmaf(w, v3, T3);
+        }
+      }
+      if (!FIRST) {
+        float* out = Xbar + p * (int64_t)(C * I) + i;
+        out[0] = fmaf(y[0], T1, fmaf(g1, T2, g2 * T3));
+#pragma unroll
+        for (int a = 0; a < NF; ++a) {
+          float v = y[1 + a] * T1;
+          if (a < NS) v = fmaf(2.f * y[1 + NF + a] * dx[a], T2, v);
+          out[(1 + a) * I] = v;
+        }
+#pragma unroll
+        for (int a = 0; a < NS; ++a) out[(1 + NF + a) * I] = y[1 + NF + a] * T1;
+      }
+    }
+  }
+  if (MODE == LAST_JET) return;
+  // ---------------- fixed-order block reduction -> part[block][IB + 4]
+  __shared__ float red[3][LF_WARPS];
+  if (lane == 0) {
+    red[0][warp] = db;
+    red[1][warp] = sq;
+    red[2][warp] = bad;
+  }
+  __syncthreads();
+  float* dst = part + (size_t)blockIdx.x * (IB + 4);
+  for (int t = threadIdx.x; t < IB; t += 32 * LF_WARPS) {
+    float v = 0.f;
+#pragma unroll
+    for (int w = 0; w < LF_WARPS; ++w) v += acc_sh[(size_t)w * IB + t];
+    const int n = t / I, i = t - n * I;
+    dst[i * B + n] = v;                  // flat W layout [i][n]
+  }
+  if (threadIdx.x < 3) {
+    float v = 0.f;
+#pragma unroll
+    for (int w = 0; w < LF_WARPS; ++w) v += red[threadIdx.x][w];
+    dst[IB + threadIdx.x] = v;
+  }
+}
+
+// dW[t] += sum_b part[b][t] (t < IB), db += sum_b part[b][IB], out_loss += scale * sum_b part[b][IB+1]
+// (double), out_flag += sum_b part[b][IB+2]; every sum in a fixed order.
+__global__ void k_reduce_last(const float* __restrict__ part, int nb, int IB, float* __restrict__ dW,
+                              float* __restrict__ db, float scale, float* __restrict__ out_loss,
+                              float* __restrict__ out_flag) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < IB) {
+    float s = 0.f;
+    for (int b = 0; b < nb; ++b) s += part[(size_t)b * (IB + 4) + t];
+    dW[t] += s;
+  } else if (t < IB + 3) {
+    double s = 0.0;
+    for (int b = 0; b < nb; ++b) s += (double)part[(size_t)b * (IB + 4) + t];
+    if (t == IB) *db += (float)s;
+    else if (t == IB + 1) *out_loss += (float)(s * (double)scale);
+    else *out_flag += (float)s;
+  }
+}
+
+}  // namespace

@@ -1,0 +1,177 @@
+// pass_impl.cuh -- the chunked scheduler of one PINN loss+gradient (or forward-jet) pass, included by
+// pass_m<M>.cu with HRKAN_M set: forward through the hidden layers (SIMT or tcgen05), the fused
+// output-layer/loss kernel, then the reverse through the hidden layers (SURVEY §3 call stack).
+#pragma once
+#include "hrkan_internal.cuh"
+#include "simt_kernels.cuh"
+#include "last_kernels.cuh"
+#include "tc_kernels.cuh"
+
+namespace {
+
+template <int NF, int NS, int M, int MODE, bool FIRST>
+hrkan_status launch_last(hrkan_net* net, const float* in, int64_t n, const PassArgs& a, int64_t c0, float* xbar,
+                         cudaStream_t st) {
+  const int l = net->L - 1;
+  const int I = net->widths[l];
+  const int IB = I * net->B;
+  auto kfn = k_last_fused<NF, NS, M, MODE, FIRST>;
+  if (MODE == LAST_JET) {
+    const unsigned grid = (unsigned)std::min<int64_t>(8 * net->num_sms, (n + LF_WARPS - 1) / LF_WARPS);
+    HR_LAUNCH(HRKAN_K_FWD_LAST, "k_last_fused",
+              kfn<<<grid, 32 * LF_WARPS, 0, st>>>(in, net->params + net->w_off[l], net->params + net->b_off[l], n, I,
+                                                  net->bc, a.u ? a.u + c0 : nullptr, a.du ? a.du + c0 * NF : nullptr,
+                                                  a.d2u ? a.d2u + c0 * NF : nullptr, nullptr, nullptr, nullptr, 0.f,
+                                                  0.f, 0.f, 0.f, nullptr, nullptr));
+    return HRKAN_OK;
+  }
+  const size_t smem = sizeof(float) * (size_t)LF_WARPS * IB;
+  if (smem > 200 * 1024) return fail(HRKAN_EUNSUPPORTED, "output layer too wide for the fused last-layer kernel");
+  if (smem > 48 * 1024) HR_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int per_sm = std::max(1, std::min(4, (int)((220 * 1024) / std::max<size_t>(smem, 1))));
+  const int nb = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)per_sm * net->num_sms, (n + LF_WARPS - 1) / LF_WARPS));
+  HR_CUDA(net->last_part.ensure(sizeof(float) * (size_t)nb * (IB + 4)));
+  const float* pts = a.pts + c0 * net->D;
+  const float* f = a.forcing ? a.forcing + c0 : nullptr;
+  const float* g = a.g ? a.g + c0 : nullptr;
+  const hrkan_pde* pde = a.pde;
+  HR_LAUNCH(HRKAN_K_FWD_LAST, "k_last_fused",
+            kfn<<<nb, 32 * LF_WARPS, smem, st>>>(in, net->params + net->w_off[l], net->params + net->b_off[l], n, I,
+                                                 net->bc, nullptr, nullptr, nullptr, pts, f, g, pde->alpha, pde->adv,
+                                                 pde->visc, a.inv_n, xbar, net->last_part.f()));
+  const float scale = (MODE == LAST_BOUNDARY) ? a.inv_n : pde->alpha * a.inv_n;
+  HR_LAUNCH(HRKAN_K_REDUCE, "k_reduce_last",
+            k_reduce_last<<<(IB + 3 + 255) / 256, 256, 0, st>>>(net->last_part.f(), nb, IB, a.grad + net->w_off[l],
+                                                                 a.grad + net->b_off[l], scale, a.out_loss, a.out_flag));
+  return HRKAN_OK;
+}
+
+// Forward + (optional) loss/seeds + reverse over one point set, chunk by chunk.
+template <int NF, int NS, int M>
+hrkan_status run_pass(hrkan_net* net, const PassArgs& a, cudaStream_t st) {
+  constexpr int C = 1 + NF + NS;
+  const int L = net->L, D = net->D;
+  const int64_t Pc = std::min<int64_t>(auto_chunk(net), std::max<int64_t>(a.P, 1));
+  HR_TRY(ensure_workspace(net, Pc, C));
+  // layer-input jet buffers: jet[l] for l = 1..L-1 (the output layer is fused with the loss)
+  std::vector<float*> jet(L + 1, nullptr);
+  {
+    float* q = net->jets.f();
+    for (int l = 1; l <= L; ++l) {
+      jet[l] = q;
+      q += (size_t)Pc * C * net->widths[l];
+    }
+  }
+  const BasisCfg bc = net->bc;
+  for (int64_t c0 = 0; c0 < a.P; c0 += Pc) {
+    const int64_t n = std::min(Pc, a.P - c0);
+    const float* X0 = a.pts + c0 * D;
+    // ---------------- forward through the hidden layers
+    for (int l = 0; l < L - 1; ++l) {
+      const int I = net->widths[l], O = net->widths[l + 1];
+      const float* in = (l == 0) ? X0 : jet[l];
+      bool done = false;
+      if (l > 0) HR_TRY(tc_forward_layer<NF, NS, M>(net, l, in, jet[l + 1], n, st, &done));
+      if (!done) {
+        const int64_t tot = n * O;
+        const unsigned grid = (unsigned)((tot + 255) / 256);
+        const int cls = (l == 0) ? HRKAN_K_FWD_FIRST : HRKAN_K_FWD_HIDDEN;
+        if (l == 0)
+          HR_LAUNCH(cls, "k_fwd_simt", k_fwd_simt<NF, NS, M, true><<<grid, 256, 0, st>>>(in, net->wt[l], net->params + net->b_off[l], jet[l + 1], n, I, O, bc));
+        else
+          HR_LAUNCH(cls, "k_fwd_simt", k_fwd_simt<NF, NS, M, false><<<grid, 256, 0, st>>>(in, net->wt[l], net->params + net->b_off[l], jet[l + 1], n, I, O, bc));
+      }
+    }
+    // ---------------- output layer fused with residual, loss, seeds and its reverse (a3, a4, a8)
+    const float* in_last = (L == 1) ? X0 : jet[L - 1];
+    float* ybar = net->adj_a.f();
+    float* xbar = net->adj_b.f();
+    if (a.kind == PASS_JET) {
+      if constexpr (NF == NS && NF >= 1) {
+        if (L == 1) HR_TRY((launch_last<NF, NS, M, LAST_JET, true>(net, in_last, n, a, c0, nullptr, st)));
+        else HR_TRY((launch_last<NF, NS, M, LAST_JET, false>(net, in_last, n, a, c0, nullptr, st)));
+      }
+      continue;
+    }
+    auto last = [&](auto MODEc) -> hrkan_status {
+      constexpr int MODE = decltype(MODEc)::value;
+      if (L == 1) return launch_last<NF, NS, M, MODE, true>(net, in_last, n, a, c0, nullptr, st);
+      return launch_last<NF, NS, M, MODE, false>(net, in_last, n, a, c0, ybar, st);
+    };
+    if (a.kind == PASS_INTERIOR) {
+      if (a.pde->kind == HRKAN_BURGERS) {
+        if constexpr (NF == 2 && NS == 1) HR_TRY(last(std::integral_constant<int, LAST_BURGERS>{}));
+        else return fail(HRKAN_EINVAL, "internal: Burgers pass needs NF=2, NS=1");
+      } else {
+        if constexpr (NF == NS && NF >= 1) HR_TRY(last(std::integral_constant<int, LAST_POISSON>{}));
+        else return fail(HRKAN_EINVAL, "internal: Poisson pass needs NF=NS=D");
+      }
+    } else {
+      if constexpr (NF == 0 && NS == 0) HR_TRY(last(std::integral_constant<int, LAST_BOUNDARY>{}));
+      else return fail(HRKAN_EINVAL, "internal: boundary pass needs C=1");
+    }
+    // ---------------- reverse through the hidden layers (a5, a6, a7), last to first
+    for (int l = L - 2; l >= 0; --l) {
+      const int I = net->widths[l], O = net->widths[l + 1];
+      const float* in = (l == 0) ? X0 : jet[l];
+      float* dW = a.grad + net->w_off[l];
+      float* db = a.grad + net->b_off[l];
+      bool done = false;
+      if (l > 0) HR_TRY(tc_wgrad_layer<NF, NS, M>(net, l, in, ybar, dW, db, n, st, &done));
+      if (!done) {
+        const dim3 blk(WG_J, WG_I);
+        const int gx = (O + WG_J - 1) / WG_J, gy = (I + WG_I - 1) / WG_I;
+        int nz = (int)std::max<int64_t>(1, (4 * net->num_sms + gx * gy - 1) / (gx * gy));
+        nz = (int)std::min<int64_t>(nz, std::max<int64_t>(1, n / 64));
+        nz = std::min(nz, NZ_MAX);
+        const dim3 grid(gx, gy, nz);
+        const size_t smem = sizeof(float) * WG_I * net->B * WG_J;
+        const int cls = (l == 0) ? HRKAN_K_WGRAD_FIRST : HRKAN_K_WGRAD_HIDDEN;
+        if (l == 0) {
+          auto kfn = k_wgrad_simt<NF, NS, M, true>;
+          if (smem > 48 * 1024) HR_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+          HR_LAUNCH(cls, "k_wgrad_simt", kfn<<<grid, blk, smem, st>>>(in, ybar, net->w_part.f(), net->b_part.f(), n, I, O, bc));
+        } else {
+          auto kfn = k_wgrad_simt<NF, NS, M, false>;
+          if (smem > 48 * 1024) HR_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+          HR_LAUNCH(cls, "k_wgrad_simt", kfn<<<grid, blk, smem, st>>>(in, ybar, net->w_part.f(), net->b_part.f(), n, I, O, bc));
+        }
+        const int64_t nW = (int64_t)O * I * net->B;
+        HR_LAUNCH(HRKAN_K_REDUCE, "k_reduce_parts",
+                  k_reduce_parts<<<(unsigned)((nW + O + 255) / 256), 256, 0, st>>>(net->w_part.f(), net->b_part.f(), nz, nW, O, dW, db));
+      }
+      if (l > 0) {
+        bool ddone = false;
+        HR_TRY(tc_dgrad_layer<NF, NS, M>(net, l, in, ybar, xbar, n, st, &ddone));
+        if (!ddone) {
+          const int64_t tot = n * I;
+          HR_LAUNCH(HRKAN_K_DGRAD_HIDDEN, "k_dgrad_simt",
+                    k_dgrad_simt<NF, NS, M><<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(in, net->params + net->w_off[l], ybar, xbar, n, I, O, bc));
+        }
+        std::swap(ybar, xbar);
+      }
+    }
+  }
+  return HRKAN_OK;
+}
+
+template <class F>
+hrkan_status with_channels(int nf, int ns, F&& f) {
+  if (nf == 0 && ns == 0) return f(IC<0>{}, IC<0>{});
+  if (nf == 1 && ns == 1) return f(IC<1>{}, IC<1>{});
+  if (nf == 2 && ns == 1) return f(IC<2>{}, IC<1>{});
+  if (nf == 2 && ns == 2) return f(IC<2>{}, IC<2>{});
+  if (nf == 3 && ns == 3) return f(IC<3>{}, IC<3>{});
+  return fail(HRKAN_EINVAL, "internal: unsupported channel set");
+}
+
+}  // namespace
+
+#define HRKAN_DEFINE_DISPATCH(MM)                                                                   \
+  namespace hrkan {                                                                                \
+  hrkan_status dispatch_pass_m##MM(hrkan_net* net, int nf, int ns, const PassArgs& a, cudaStream_t st) { \
+    return with_channels(nf, ns, [&](auto NFc, auto NSc) {                                        \
+      return run_pass<decltype(NFc)::value, decltype(NSc)::value, MM>(net, a, st);                \
+    });                                                                                            \
+  }                                                                                                \
+  }

@@ -11,7 +11,8 @@
 #pragma once
 #include "hr_basis.cuh"
 
-namespace hrkan {
+namespace {   // internal linkage: every translation unit owns its kernels
+using namespace hrkan;
 
 template <int NF, int NS>
 struct Ch {
@@ -452,4 +453,4 @@ __global__ void k_init_layer(float* __restrict__ W, float* __restrict__ b, int64
   if (t < O) b[t] = 0.f;
 }
 
-}  // namespace hrkan
+}  // namespace
