@@ -5,6 +5,8 @@
 // Every arithmetic step of the hot path runs in the kernels of simt_kernels.cuh, last_kernels.cuh
 // and tc_*.cuh; this file only validates arguments, owns device memory and sequences launches on
 // the caller's stream (SURVEY §3 "New build" call stack).
+#include <cstdlib>
+
 #include "hrkan_internal.cuh"
 #include "simt_kernels.cuh"
 #include "tc_kernels.cuh"   // weight tiling for the tensor-core engine (tc_refresh_weights, tc_free)
@@ -129,6 +131,9 @@ hrkan_status hrkan_create(const int32_t* widths, int32_t n_widths, int32_t G, in
     net->max_width = std::max(net->max_width, widths[l + 1]);
   }
   net->n_params = off;
+  // tuning overrides for experiments (precision/speed trade-off of the TMEM drain segments)
+  if (const char* e = std::getenv("HRKAN_TC_SEG")) net->tc_seg = std::max(1, std::atoi(e));
+  if (const char* e = std::getenv("HRKAN_TC_WSEG")) net->tc_wseg = std::max(1, std::atoi(e));
   auto cleanup = [&](hrkan_status s) {
     hrkan_free(net);
     return s;

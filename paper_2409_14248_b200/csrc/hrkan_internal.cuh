@@ -2,6 +2,7 @@
 // libhrkan.so (hrkan_abi.cu: the C ABI; pass_m<M>.cu: the chunked loss+gradient scheduler
 // instantiated for HR order M, compiled in parallel).
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -133,6 +134,41 @@ struct hrkan_net {
 namespace hrkan {
 
 constexpr int NZ_MAX = 64;
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link dependency).
+using PFN_tmapEncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                         const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                         CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+inline PFN_tmapEncodeTiled tmap_encoder() {
+  static PFN_tmapEncodeTiled fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_tmapEncodeTiled>(f);
+    else
+      cudaGetLastError();
+  }
+  return fn;
+}
+
+// fp32 3-D tensor map over a row-major [d2][d1][d0] array (d0 innermost), box b0 x b1 x b2, no swizzle,
+// zero fill out of bounds.  Requires 16-B aligned base and d0*4, d0*d1*4 multiples of 16.
+inline hrkan_status make_tmap_f32_3d(CUtensorMap* m, const float* base, uint64_t d0, uint64_t d1, uint64_t d2,
+                                     uint32_t b0, uint32_t b1, uint32_t b2) {
+  PFN_tmapEncodeTiled enc = tmap_encoder();
+  if (!enc) return fail(HRKAN_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t dims[3] = {d0, d1, d2};
+  const cuuint64_t strides[2] = {d0 * 4, d0 * d1 * 4};
+  const cuuint32_t box[3] = {b0, b1, b2};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  const CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides, box, estr,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(HRKAN_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  return HRKAN_OK;
+}
 
 inline int prof_pre(hrkan_net* net, cudaStream_t st) {
   if (!net->prof_on) return -1;

@@ -16,7 +16,8 @@
 
 namespace {
 
-__host__ __device__ constexpr int dgr_slice_p(int C) { return C == 1 ? 64 : 8; }
+__host__ __device__ constexpr int dgr_slice_p(int C) { return C == 1 ? 64 : 16; }
+constexpr int DGR_SST = 129;   // column stride of the epilogue slice (odd: conflict-free gathers)
 
 template <int NF, int NS, int M, int OT>
 struct DgrCfg {
@@ -28,9 +29,9 @@ struct DgrCfg {
   static constexpr int W_STAGE_FLOATS = 2 * 128 * TC_KB;
   static constexpr int Y_STAGE_FLOATS = 2 * N * TC_KB;
   static constexpr int SLICE_P = dgr_slice_p(C);
-  static constexpr int S_FLOATS = SLICE_P * C * 128;
+  static constexpr int S_FLOATS = SLICE_P * C * DGR_SST;
   static constexpr int STAGE_BYTES = 4 * (W_STAGE_FLOATS + Y_STAGE_FLOATS);
-  static constexpr int NSTAGE = (4 * STAGE_BYTES + 4 * S_FLOATS + 1024 <= 220 * 1024) ? 4 : 3;
+  static constexpr int NSTAGE = (4 * STAGE_BYTES + 4 * S_FLOATS + 1024 <= 220 * 1024) ? 4 : (3 * STAGE_BYTES + 4 * S_FLOATS + 1024 <= 220 * 1024) ? 3 : 2;
   static constexpr int SMEM_BYTES = NSTAGE * STAGE_BYTES + 4 * S_FLOATS + 1024;
   static constexpr uint32_t TMEM_COLS = tc_tmem_cols(2 * N);
   static_assert(N % 16 == 0 && N <= 256, "bad N");
@@ -99,7 +100,7 @@ __global__ void __launch_bounds__(DGR_THREADS, 1)
     constexpr int NTASK = N * (TC_KB / 4);
     constexpr int TPT = (NTASK + TC_GEN_THREADS - 1) / TC_GEN_THREADS;
     const int tid = threadIdx.x;
-    float4 buf[2][TPT];
+    float4 buf[3][TPT];
     auto prefetch = [&](int g, auto SLOT) {
       constexpr int sl = decltype(SLOT)::value;
       const int kb = g % NKB;
@@ -116,7 +117,7 @@ __global__ void __launch_bounds__(DGR_THREADS, 1)
     };
     auto step = [&](int g, auto SLOT) {
       constexpr int sl = decltype(SLOT)::value;
-      prefetch(g + 1, std::integral_constant<int, sl ^ 1>{});
+      prefetch(g + 2, std::integral_constant<int, (sl + 2) % 3>{});   // two blocks ahead
       const int s = g % NSTAGE;
       tc::mbar_wait(&empty_bar[s], ((g / NSTAGE) & 1) ^ 1);
       float* y_hi = smem + s * (Cfg::W_STAGE_FLOATS + Cfg::Y_STAGE_FLOATS) + Cfg::W_STAGE_FLOATS;
@@ -138,9 +139,11 @@ __global__ void __launch_bounds__(DGR_THREADS, 1)
       tc::mbar_arrive(&full_bar[s]);
     };
     prefetch(0, std::integral_constant<int, 0>{});
-    for (int g = 0; g < nblk; g += 2) {
+    prefetch(1, std::integral_constant<int, 1>{});
+    for (int g = 0; g < nblk; g += 3) {
       step(g, std::integral_constant<int, 0>{});
       if (g + 1 < nblk) step(g + 1, std::integral_constant<int, 1>{});
+      if (g + 2 < nblk) step(g + 2, std::integral_constant<int, 2>{});
     }
   } else if (warp < DGR_MMA_WARP) {
     // ===================== epilogue: per M-tile, TMEM -> smem slices -> jet-chain gather
@@ -160,7 +163,7 @@ __global__ void __launch_bounds__(DGR_THREADS, 1)
           float v[8];
           tc::tmem_ld8(tb + c8, v);
 #pragma unroll
-          for (int q = 0; q < 8; ++q) S[(c8 + q) * 128 + r] = v[q];
+          for (int q = 0; q < 8; ++q) S[(c8 + q) * DGR_SST + r] = v[q];
         }
         if (sl == NP / SLICE_P - 1) {             // accumulator fully read: release it early
           tc::tc_fence_before();
@@ -180,7 +183,7 @@ __global__ void __launch_bounds__(DGR_THREADS, 1)
           for (int a = 0; a < NF; ++a) dxb[a] = 0.f;
 #pragma unroll
           for (int a = 0; a < NS; ++a) ddxb[a] = 0.f;
-          const float* Sp = S + (pq * C) * 128 + il * bc.B;
+          const float* Sp = S + (pq * C) * DGR_SST + il * bc.B;
 #pragma unroll
           for (int rr = 0; rr < KMAX; ++rr) {
             if (rr > bc.k) break;
@@ -190,7 +193,7 @@ __global__ void __launch_bounds__(DGR_THREADS, 1)
             hr_eval<M, (NS > 0 ? 3 : 2)>(basis_q(x, n, bc), bc.sc, v0, v1, v2, v3);
             float ab[C];
 #pragma unroll
-            for (int c = 0; c < C; ++c) ab[c] = Sp[c * 128 + n];
+            for (int c = 0; c < C; ++c) ab[c] = Sp[c * DGR_SST + n];
             xb = fmaf(ab[0], v1, xb);
 #pragma unroll
             for (int a = 0; a < NF; ++a) {

@@ -13,10 +13,12 @@
 //   MMA N = NP points x C channels of one point tile (channel-major columns n = c*NP + p),
 //   MMA K = I*B (dense over all bases, zero-padded to a multiple of KB).
 //   smem stage = { W_hi, W_lo tiles [KB/4 chunks][O rows][4] via one 1-D bulk copy of a
-//                  pre-tiled global copy;  A_hi, A_lo tiles [KB/4][N][4] written by 4 generator
-//                  warps from the jet }, NSTAGE-deep mbarrier ring.
-//   warps 0-3: generators, then epilogue (TMEM -> registers -> +bias -> Y[p][c][o], coalesced);
-//   warp 4: TMEM allocator + single-thread MMA issuer; warp 5: bulk-copy producer.
+//                  pre-tiled global copy;  A_hi, A_lo tiles [KB/4][N][4] written by the generator
+//                  warps }, NSTAGE-deep mbarrier ring.  The generators read the saved input jet from
+//   a ring of TMA-loaded windows X[tile points][C][8 inputs] (coalesced, prefetched ahead).
+//   warps 0-7: two generator groups (alternate K-blocks), then the segment drains (TMEM -> +bias ->
+//   Y[p][c][o], coalesced); warp 8: TMEM allocator + single-thread MMA issuer; warp 9: W bulk copies;
+//   warp 10: jet-window TMA loads.
 #pragma once
 #include "tc_ptx.cuh"
 
@@ -25,11 +27,12 @@ namespace {
 using namespace hrkan;
 
 constexpr int TC_KB = 16;          // K per pipeline stage (two tf32 MMA K-steps of 8)
-constexpr int TC_NSTAGE = 3;
 constexpr int TC_GEN_THREADS = 128;   // one generator group (4 warps); the group handles every other K-block
-constexpr int TC_NGEN = 2;            // generator groups (group 0 also drains the accumulators)
-constexpr int TC_THREADS = 32 * (4 * TC_NGEN + 2);   // + MMA warp + producer warp
-constexpr int TC_MMA_WARP = 4 * TC_NGEN, TC_PROD_WARP = 4 * TC_NGEN + 1;
+constexpr int TC_NGEN = 2;            // generator groups (both also drain the accumulators)
+constexpr int TC_MMA_WARP = 4 * TC_NGEN, TC_PROD_WARP = 4 * TC_NGEN + 1, TC_WIN_WARP = 4 * TC_NGEN + 2;
+constexpr int TC_THREADS = 32 * (4 * TC_NGEN + 3);   // + MMA warp + W producer warp + jet-window TMA warp
+constexpr int TC_WIN = 8;             // inputs per jet window
+constexpr int TC_NWIN = 4;            // jet-window ring depth
 
 // Points per tile so that N = NP*C is a multiple of 16 and <= 256.
 __host__ __device__ constexpr int tc_np(int C) {
@@ -46,14 +49,23 @@ struct FwdCfg {
   static constexpr int NP = tc_np(C);
   static constexpr int N = NP * C;
   static constexpr int O = 128 * NMT;
-  static constexpr int W_STAGE_FLOATS = 2 * O * TC_KB;     // hi + lo
-  static constexpr int A_STAGE_FLOATS = 2 * N * TC_KB;
-  static constexpr int STAGE_BYTES = 4 * (W_STAGE_FLOATS + A_STAGE_FLOATS);
-  static constexpr int SMEM_BYTES = TC_NSTAGE * STAGE_BYTES + 1024;
+  // generated operand: [KB/4 chunks][N rows][4], chunk stride padded to 32 B (mod 128 B) so that the
+  // generators' (chunk-fastest) float4 stores are bank-conflict free
+  static constexpr int ACS = N * 4 + 8;                      // chunk stride (floats)
+  static constexpr int W_STAGE_FLOATS = 2 * O * TC_KB;       // hi + lo, [KB/4][O][4] each
+  static constexpr int A_STAGE_FLOATS = 2 * (TC_KB / 4) * ACS;
+  static constexpr int STAGE_FLOATS = W_STAGE_FLOATS + A_STAGE_FLOATS;
+  static constexpr int STAGE_BYTES = 4 * STAGE_FLOATS;
+  static constexpr int WIN_FLOATS = NP * C * TC_WIN;         // TMA box [NP points][C][TC_WIN inputs]
+  static constexpr int FIXED_BYTES = 4 * TC_NWIN * WIN_FLOATS + 4 * 256 + 1024;
+  static constexpr int NSTAGE_FIT = (225 * 1024 - FIXED_BYTES) / STAGE_BYTES;   // static smem + margin
+  static constexpr int NSTAGE = NSTAGE_FIT > 4 ? 4 : NSTAGE_FIT;
+  static constexpr int SMEM_BYTES = NSTAGE * STAGE_BYTES + FIXED_BYTES;
   static constexpr int NACC = (2 * NMT * N <= 512) ? 2 : 1;   // double-buffered accumulators if they fit
   static constexpr uint32_t TMEM_COLS = tc_tmem_cols(NACC * NMT * N);
   static_assert(N % 16 == 0 && N <= 256, "bad N");
   static_assert(NMT * N <= 512, "accumulators exceed TMEM");
+  static_assert(NSTAGE >= 2, "shared memory budget");
 };
 
 // Pre-tiled, pre-split weights for k_fwd_tc: for K-block kb: [hi | lo] each [KB/4][O][4].
@@ -73,24 +85,35 @@ __global__ void k_tile_w_fwd(const float* __restrict__ W, float* __restrict__ Wt
   dst[per_kb + r] = lo;
 }
 
+// Forward hidden layer.  Warp roles:
+//   warps 0..7   two generator groups (K-blocks kb = grp mod 2), then the segment drains;
+//   warp 8       TMEM allocator + single-thread tcgen05.mma issuer;
+//   warp 9       1-D bulk copies of the pre-tiled W_hi/W_lo stage;
+//   warp 10      TMA loads of jet windows: X[p0 .. p0+NP)[C][8w .. 8w+8) -> smem ring (TC_NWIN deep),
+//                so the generators read the jets from shared memory (coalesced, latency hidden).
 template <int NF, int NS, int M, int NMT>
 __global__ void __launch_bounds__(TC_THREADS, 1)
-    k_fwd_tc(const float* __restrict__ X, const float* __restrict__ Wtiled, const float* __restrict__ bias,
+    k_fwd_tc(const __grid_constant__ CUtensorMap tmX, const float* __restrict__ Wtiled, const float* __restrict__ bias,
              float* __restrict__ Y, int64_t P, int I, int nkb, int seg, BasisCfg bc) {
   using Cfg = FwdCfg<NF, NS, M, NMT>;
-  constexpr int C = Cfg::C, NP = Cfg::NP, N = Cfg::N, O = Cfg::O, NACC = Cfg::NACC;
+  constexpr int C = Cfg::C, NP = Cfg::NP, N = Cfg::N, O = Cfg::O, NACC = Cfg::NACC, NSTAGE = Cfg::NSTAGE;
+  constexpr int ACS = Cfg::ACS;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   float* smem = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ __align__(8) uint64_t full_bar[TC_NSTAGE], empty_bar[TC_NSTAGE], acc_full[NACC], acc_empty[NACC];
+  float* win = smem + NSTAGE * Cfg::STAGE_FLOATS;            // [TC_NWIN][NP][C][TC_WIN]
+  float* ctr = win + TC_NWIN * Cfg::WIN_FLOATS;              // basis centres mid_n, n < B
+  __shared__ __align__(8) uint64_t full_bar[NSTAGE], empty_bar[NSTAGE], acc_full[NACC], acc_empty[NACC];
+  __shared__ __align__(8) uint64_t win_full[TC_NWIN], win_empty[TC_NWIN];
   __shared__ uint32_t tmem_base_sh;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t p0 = (int64_t)blockIdx.x * NP;
   const int K = I * bc.B;
   const int nseg = (nkb + seg - 1) / seg;
+  const int nwin = (I + TC_WIN - 1) / TC_WIN;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < TC_NSTAGE; ++s) {
+    for (int s = 0; s < NSTAGE; ++s) {
       tc::mbar_init(&full_bar[s], TC_GEN_THREADS + 1);
       tc::mbar_init(&empty_bar[s], 1);
     }
@@ -98,8 +121,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       tc::mbar_init(&acc_full[a], 1);
       tc::mbar_init(&acc_empty[a], TC_GEN_THREADS * TC_NGEN);
     }
+    for (int w = 0; w < TC_NWIN; ++w) {
+      tc::mbar_init(&win_full[w], 1);
+      tc::mbar_init(&win_empty[w], 4 * TC_NGEN);           // one elected lane per generator warp
+    }
     tc::fence_mbar_init();
   }
+  for (int n = threadIdx.x; n < bc.B; n += blockDim.x) ctr[n] = fmaf((float)n, bc.h, bc.mid0);
   if (warp == TC_MMA_WARP) tc::tmem_alloc<Cfg::TMEM_COLS>(&tmem_base_sh);
   tc::tc_fence_before();
   __syncthreads();
@@ -153,77 +181,78 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       tc::mbar_arrive(&acc_empty[buf]);
     };
     // ===================== generators: A^c[p, k] for the stage's KB columns.
-    // Each thread owns TPT tasks (point pl, 4-wide K chunk j) per block; the jets of the next
-    // block are prefetched into registers while the current block is generated.
+    // Task = (point pl, 4-wide K chunk j), chunk fastest across lanes; the jets come from the TMA
+    // window ring.  K positions advance incrementally (no integer division in the loop).
     constexpr int NTASK = NP * (TC_KB / 4);
     constexpr int TPT = (NTASK + TC_GEN_THREADS - 1) / TC_GEN_THREADS;
-    float jx[2][TPT][2], jdx[2][TPT][2][NF > 0 ? NF : 1], jddx[2][TPT][2][NS > 0 ? NS : 1];
-    auto prefetch = [&](int kb, auto SLOT) {
-      constexpr int slot = decltype(SLOT)::value;
-#pragma unroll
-      for (int u = 0; u < TPT; ++u) {
-        const int task = gtid + u * TC_GEN_THREADS;
-        const int pl = task % NP, j = task / NP;
-        const int64_t p = p0 + pl;
-        const int k0 = kb * TC_KB + 4 * j;
-        const int i0 = k0 / bc.B;
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int i = i0 + h;
-          jx[slot][u][h] = 0.f;
-#pragma unroll
-          for (int a = 0; a < NF; ++a) jdx[slot][u][h][a] = 0.f;
-#pragma unroll
-          for (int a = 0; a < NS; ++a) jddx[slot][u][h][a] = 0.f;
-          if (task < NTASK && p < P && i < I && kb < nkb) {
-            const float* base = X + p * (int64_t)(C * I) + i;
-            jx[slot][u][h] = __ldg(base);
-#pragma unroll
-            for (int a = 0; a < NF; ++a) jdx[slot][u][h][a] = __ldg(base + (1 + a) * I);
-#pragma unroll
-            for (int a = 0; a < NS; ++a) jddx[slot][u][h][a] = __ldg(base + (1 + NF + a) * I);
-          }
-        }
-      }
-    };
+    const int j = gtid & 3;                    // fixed chunk of this thread (TC_GEN_THREADS % 4 == 0)
+    const int B = bc.B;
+    int i0, n0;                                // task K position k0 = kb*KB + 4j -> (input i0, basis n0)
+    int ilo, nlo;                              // K-block start kb*KB -> (ilo, nlo)
+    {
+      const int k0 = grp * TC_KB + 4 * j;
+      i0 = k0 / B;
+      n0 = k0 - i0 * B;
+      ilo = (grp * TC_KB) / B;
+      nlo = grp * TC_KB - ilo * B;
+    }
+    const int dstep = TC_KB * TC_NGEN;         // K advance per group step
+    const int di = dstep / B, dn = dstep - (dstep / B) * B;
+    int wwait = 0, wrel = 0;                   // next window to wait for / to release
     int next_drain = 0;
-    // one K-block: prefetch the group's next block into the other register slot, then generate
-    auto step = [&](int kb, auto SLOT) {
-      constexpr int slot = decltype(SLOT)::value;
-      while (next_drain < nseg - 1 && kb >= (next_drain + 1) * seg + TC_NSTAGE) drain(next_drain++);
-      prefetch(kb + TC_NGEN, std::integral_constant<int, slot ^ 1>{});
-      const int s = kb % TC_NSTAGE;
-      const uint32_t ph = (kb / TC_NSTAGE) & 1;
-      tc::mbar_wait(&empty_bar[s], ph ^ 1);
-      float* a_hi = smem + s * (Cfg::W_STAGE_FLOATS + Cfg::A_STAGE_FLOATS) + Cfg::W_STAGE_FLOATS;
-      float* a_lo = a_hi + N * TC_KB;
+    for (int kb = grp; kb < nkb; kb += TC_NGEN) {
+      while (next_drain < nseg - 1 && kb >= (next_drain + 1) * seg + NSTAGE) drain(next_drain++);
+      // windows: release those below this K-block's first input, wait for those up to its last
+      const int ihi = min(I - 1, ilo + (nlo + TC_KB - 1 >= B) + (nlo + TC_KB - 1 >= 2 * B));
+      while (wrel < (ilo >> 3)) {
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&win_empty[wrel % TC_NWIN]);
+        ++wrel;
+      }
+      while (wwait <= (ihi >> 3)) {
+        tc::mbar_wait(&win_full[wwait % TC_NWIN], (uint32_t)((wwait / TC_NWIN) & 1));
+        ++wwait;
+      }
+      const int s = kb % NSTAGE;
+      tc::mbar_wait(&empty_bar[s], ((kb / NSTAGE) & 1) ^ 1);
+      float* a_hi = smem + s * Cfg::STAGE_FLOATS + Cfg::W_STAGE_FLOATS;
+      float* a_lo = a_hi + (TC_KB / 4) * ACS;
 #pragma unroll
       for (int u = 0; u < TPT; ++u) {
         const int task = gtid + u * TC_GEN_THREADS;
         if (task >= NTASK) break;
-        const int pl = task % NP, j = task / NP;
-        const int k0 = kb * TC_KB + 4 * j;
-        const int i0 = k0 / bc.B;
-        int n = k0 - i0 * bc.B;
+        const int pl = task >> 2;
+        // jets of inputs i0 and i0+1 (the chunk crosses into i0+1 when n0 + 3 >= B)
+        float jx[2], jdx[2][NF > 0 ? NF : 1], jddx[2][NS > 0 ? NS : 1];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int i = i0 + h;
+          const float* wp = win + ((i >> 3) % TC_NWIN) * Cfg::WIN_FLOATS + (pl * C) * TC_WIN + (i & 7);
+          jx[h] = wp[0];
+#pragma unroll
+          for (int a = 0; a < NF; ++a) jdx[h][a] = wp[(1 + a) * TC_WIN];
+#pragma unroll
+          for (int a = 0; a < NS; ++a) jddx[h][a] = wp[(1 + NF + a) * TC_WIN];
+        }
         float va[C][4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          const bool h = n >= bc.B;                   // chunk crosses into input i0+1
-          const int nn = h ? n - bc.B : n;
-          const float x = h ? jx[slot][u][1] : jx[slot][u][0];
+          const int n = n0 + e;
+          const bool h = n >= B;                      // chunk crosses into input i0+1
+          const int nn = h ? n - B : n;
+          const float x = h ? jx[1] : jx[0];
           float v0, v1, v2, v3;
-          hr_eval<M, (NS > 0 ? 2 : 1)>(basis_q(x, nn, bc), bc.sc, v0, v1, v2, v3);
-          if (k0 + e >= K) v0 = v1 = v2 = 0.f;
+          hr_eval<M, (NS > 0 ? 2 : 1)>((x - ctr[nn]) * bc.sc, bc.sc, v0, v1, v2, v3);
+          if (i0 * B + n >= K) v0 = v1 = v2 = 0.f;
           va[0][e] = v0;
 #pragma unroll
-          for (int a = 0; a < NF; ++a) va[1 + a][e] = v1 * (h ? jdx[slot][u][1][a] : jdx[slot][u][0][a]);
+          for (int a = 0; a < NF; ++a) va[1 + a][e] = v1 * (h ? jdx[1][a] : jdx[0][a]);
 #pragma unroll
           for (int a = 0; a < NS; ++a) {
-            const float d1 = h ? jdx[slot][u][1][a] : jdx[slot][u][0][a];
-            const float d2 = h ? jddx[slot][u][1][a] : jddx[slot][u][0][a];
+            const float d1 = h ? jdx[1][a] : jdx[0][a];
+            const float d2 = h ? jddx[1][a] : jddx[0][a];
             va[1 + NF + a][e] = fmaf(v2 * d1, d1, v1 * d2);
           }
-          ++n;
         }
 #pragma unroll
         for (int c = 0; c < C; ++c) {
@@ -233,17 +262,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           tc::split_tf32(va[c][2], hh.z, ll.z);
           tc::split_tf32(va[c][3], hh.w, ll.w);
           const int row = c * NP + pl;                  // channel-major columns of the MMA N
-          *reinterpret_cast<float4*>(a_hi + (j * N + row) * 4) = hh;
-          *reinterpret_cast<float4*>(a_lo + (j * N + row) * 4) = ll;
+          *reinterpret_cast<float4*>(a_hi + j * ACS + row * 4) = hh;
+          *reinterpret_cast<float4*>(a_lo + j * ACS + row * 4) = ll;
         }
       }
       tc::fence_proxy_async_smem();
       tc::mbar_arrive(&full_bar[s]);
-    };
-    prefetch(grp, std::integral_constant<int, 0>{});
-    for (int kb = grp; kb < nkb; kb += 2 * TC_NGEN) {
-      step(kb, std::integral_constant<int, 0>{});
-      if (kb + TC_NGEN < nkb) step(kb + TC_NGEN, std::integral_constant<int, 1>{});
+      // advance to this group's next K-block
+      n0 += dn; i0 += di;
+      if (n0 >= B) { n0 -= B; ++i0; }
+      nlo += dn; ilo += di;
+      if (nlo >= B) { nlo -= B; ++ilo; }
     }
     while (next_drain < nseg) drain(next_drain++);
   } else if (warp == TC_MMA_WARP) {
@@ -257,20 +286,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           tc::mbar_wait(&acc_empty[buf], (uint32_t)((sg / NACC - 1) & 1));
           tc::tc_fence_after();
         }
-        const int s = kb % TC_NSTAGE;
-        const uint32_t ph = (kb / TC_NSTAGE) & 1;
-        tc::mbar_wait(&full_bar[s], ph);
+        const int s = kb % NSTAGE;
+        tc::mbar_wait(&full_bar[s], (kb / NSTAGE) & 1);
         tc::tc_fence_after();
-        const float* w_hi = smem + s * (Cfg::W_STAGE_FLOATS + Cfg::A_STAGE_FLOATS);
+        const float* w_hi = smem + s * Cfg::STAGE_FLOATS;
         const float* w_lo = w_hi + O * TC_KB;
         const float* a_hi = w_hi + Cfg::W_STAGE_FLOATS;
-        const float* a_lo = a_hi + N * TC_KB;
+        const float* a_lo = a_hi + (TC_KB / 4) * ACS;
 #pragma unroll
         for (int ks = 0; ks < TC_KB / 8; ++ks) {
-          // K-step ks covers chunks 2ks, 2ks+1: LBO = chunk stride = rows*16 B, SBO = 8 rows = 128 B
-          const uint32_t aoff = (uint32_t)(2 * ks * N * 16);
-          const uint64_t bh = tc::smem_desc(tc::smem_u32(a_hi) + aoff, N * 16, 128);
-          const uint64_t bl = tc::smem_desc(tc::smem_u32(a_lo) + aoff, N * 16, 128);
+          // K-step ks covers chunks 2ks, 2ks+1: LBO = chunk stride, SBO = 8 rows = 128 B
+          const uint32_t aoff = (uint32_t)(2 * ks * ACS * 4);
+          const uint64_t bh = tc::smem_desc(tc::smem_u32(a_hi) + aoff, ACS * 4, 128);
+          const uint64_t bl = tc::smem_desc(tc::smem_u32(a_lo) + aoff, ACS * 4, 128);
 #pragma unroll
           for (int t = 0; t < NMT; ++t) {
             const uint32_t woff = (uint32_t)(2 * ks * O * 16 + t * 128 * 16);
@@ -288,16 +316,27 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       }
     }
     __syncwarp();
-  } else {
+  } else if (warp == TC_PROD_WARP) {
     // ===================== bulk-copy producer of the pre-tiled W_hi/W_lo stage
     if (lane == 0) {
       for (int kb = 0; kb < nkb; ++kb) {
-        const int s = kb % TC_NSTAGE;
-        const uint32_t ph = (kb / TC_NSTAGE) & 1;
-        tc::mbar_wait(&empty_bar[s], ph ^ 1);
-        float* w_dst = smem + s * (Cfg::W_STAGE_FLOATS + Cfg::A_STAGE_FLOATS);
+        const int s = kb % NSTAGE;
+        tc::mbar_wait(&empty_bar[s], ((kb / NSTAGE) & 1) ^ 1);
+        float* w_dst = smem + s * Cfg::STAGE_FLOATS;
         tc::mbar_arrive_expect_tx(&full_bar[s], Cfg::W_STAGE_FLOATS * 4);
         tc::bulk_g2s(w_dst, Wtiled + (int64_t)kb * Cfg::W_STAGE_FLOATS, Cfg::W_STAGE_FLOATS * 4, &full_bar[s]);
+      }
+    }
+    __syncwarp();
+  } else {
+    // ===================== TMA producer of the jet windows
+    if (lane == 0) {
+      tc::tma_prefetch_desc(&tmX);
+      for (int w = 0; w < nwin; ++w) {
+        const int slot = w % TC_NWIN;
+        if (w >= TC_NWIN) tc::mbar_wait(&win_empty[slot], (uint32_t)(((w / TC_NWIN) - 1) & 1));
+        tc::mbar_arrive_expect_tx(&win_full[slot], Cfg::WIN_FLOATS * 4);
+        tc::tma_load_3d(win + slot * Cfg::WIN_FLOATS, &tmX, w * TC_WIN, 0, (int)p0, &win_full[slot]);
       }
     }
     __syncwarp();
@@ -324,7 +363,8 @@ bool tc_layer_ok(const hrkan_net* net, int l) {
   const int O = net->widths[l + 1], I = net->widths[l];
   if (O != 128 && O != 256) return false;
   if (net->engine == 0 && (int64_t)I * net->B < 256) return false;   // K too small to pay off
-  if (net->B < 4) return false;                   // a 4-wide K chunk spans at most 2 inputs
+  if (net->B < 8) return false;                   // a K chunk spans at most 2 inputs; <= 17 inputs per M-tile
+  if (I % 8 != 0) return false;                    // jet windows of 8 inputs (TMA rows 16-B aligned)
   return true;
 }
 
@@ -367,12 +407,15 @@ hrkan_status launch_fwd_tc(hrkan_net* net, int l, const float* X, float* Y, int6
     HR_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
     attr_set = true;
   }
+  const int I = net->widths[l];
+  CUtensorMap tm;
+  HR_TRY(make_tmap_f32_3d(&tm, X, (uint64_t)I, (uint64_t)Cfg::C, (uint64_t)n, TC_WIN, Cfg::C, Cfg::NP));
   const TcLayerState& ls = net->tc_layers[l];
   const unsigned grid = (unsigned)((n + Cfg::NP - 1) / Cfg::NP);
   const int cls = HRKAN_K_FWD_HIDDEN;
   HR_LAUNCH(cls, "k_fwd_tc",
-            kfn<<<grid, TC_THREADS, Cfg::SMEM_BYTES, st>>>(X, ls.w_fwd, net->params + net->b_off[l], Y, n,
-                                                           net->widths[l], ls.nkb, Cfg::NACC == 2 ? net->tc_seg : 2 * net->tc_seg, net->bc));
+            kfn<<<grid, TC_THREADS, Cfg::SMEM_BYTES, st>>>(tm, ls.w_fwd, net->params + net->b_off[l], Y, n, I, ls.nkb,
+                                                           Cfg::NACC == 2 ? net->tc_seg : 2 * net->tc_seg, net->bc));
   return HRKAN_OK;
 }
 

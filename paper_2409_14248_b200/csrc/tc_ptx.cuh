@@ -4,6 +4,7 @@
 // (shared-memory matrix descriptor and 32-bit instruction descriptor).
 #pragma once
 #include <cstdint>
+#include <cuda.h>            // CUtensorMap (type only; the encoder is fetched through the runtime)
 #include <cuda_runtime.h>
 
 namespace hrkan {
@@ -49,6 +50,21 @@ __device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src_gmem, u
                    smem_u32(dst_smem)),
                "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
+}
+
+// ------------------------------------------------------------------ TMA tensor copy global -> smem
+// 3-D tiled box (coordinates innermost first); out-of-bounds elements are zero-filled and still
+// count towards the transaction bytes.
+__device__ __forceinline__ void tma_load_3d(void* dst_smem, const CUtensorMap* tmap, int c0, int c1, int c2,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
+          "r"(smem_u32(dst_smem)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* tmap) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tmap)) : "memory");
 }
 
 // ------------------------------------------------------------------ TMEM

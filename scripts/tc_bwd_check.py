@@ -30,6 +30,13 @@ for key in keys:
                             {"kind": w.pde, "alpha": w.alpha, "adv": w.adv, "visc": w.visc}, ps.interior, bi, gbi)
     flat = O.flat_grad(g)
     npar = w.num_params()
+    ou, odu, od2u = O.forward_jet(O.Net(w.widths, w.G, w.k, w.m), params, ps.interior[:2048])
+    for eng in (1, 2):
+        net = HRKANNet(w.widths, w.G, w.k, w.m)
+        net.set_params(HI.flatten_params(params))
+        net.set_engine(eng)
+        gu, gdu, gd2u = [t.cpu().numpy() for t in net.forward_jet(torch.from_numpy(ps.interior[:2048]).cuda())]
+        print(key, "engine", eng, "forward u %.2e du %.2e d2u %.2e" % (rel(gu, ou), rel(gdu, odu), rel(gd2u, od2u)), flush=True)
     for eng in (1, 2):
         o = outs[eng]
         gl = HI.unflatten_params(o[:npar].copy(), w.widths, w.B)
