@@ -8,16 +8,18 @@
 //
 // Orientation: MMA M = rows (i,n) of an INPUT-ALIGNED tile (IPT = floor(128/B) whole inputs, so every
 // sum over n closes inside one tile), MMA N = (point, channel) columns p*C + c of NP points, MMA
-// K = o.  A = pre-tiled W^T hi/lo (one 1-D bulk copy per stage), B = Ybar hi/lo (loaded + split by
-// 4 generator warps, next block prefetched in registers).  Two TMEM accumulators: the 4 epilogue
-// warps drain M-tile t while the MMA runs t+1.  Epilogue: TMEM -> smem slice of SLICE_P points ->
-// each (point, input) gathers only the k+1 non-zero bases of its x -> Xbar[p][c][i].
+// K = o.  A = pre-tiled W^T hi/lo (one 1-D bulk copy per stage), B = Ybar hi/lo: the producer warp
+// TMA-loads the box Ybar[NP points][C][KB outputs] into a 2-deep ring and 4 generator warps split it
+// into the operand layout.  Two TMEM accumulators: the 4 epilogue warps drain M-tile t while the MMA
+// runs t+1.  Epilogue: TMEM -> smem slice of SLICE_P points -> each (point, input) gathers only the
+// k+1 non-zero bases of its x (input jets TMA-loaded per M-tile) -> Xbar[p][c][i].
 #pragma once
 
 namespace {
 
-__host__ __device__ constexpr int dgr_slice_p(int C) { return C == 1 ? 64 : 16; }
+__host__ __device__ constexpr int dgr_slice_p(int C) { return C == 1 ? 64 : 8; }
 constexpr int DGR_SST = 129;   // column stride of the epilogue slice (odd: conflict-free gathers)
+constexpr int DGR_IPTB = 16;   // jet box width (inputs) >= IPT + 3 (box start aligned down to 16 B), B >= 11
 
 template <int NF, int NS, int M, int OT>
 struct DgrCfg {
@@ -26,16 +28,23 @@ struct DgrCfg {
   static constexpr int N = NP * C;
   static constexpr int O = 128 * OT;
   static constexpr int NKB = O / TC_KB;
+  static constexpr int ACS = N * 4 + 8;                       // padded chunk stride of the Ybar operand
   static constexpr int W_STAGE_FLOATS = 2 * 128 * TC_KB;
-  static constexpr int Y_STAGE_FLOATS = 2 * N * TC_KB;
+  static constexpr int Y_STAGE_FLOATS = 2 * (TC_KB / 4) * ACS;
+  static constexpr int STAGE_FLOATS = W_STAGE_FLOATS + Y_STAGE_FLOATS;
+  static constexpr int RAW_FLOATS = N * TC_KB;                // TMA box Ybar[NP][C][KB]
+  static constexpr int JET_FLOATS = N * DGR_IPTB;             // TMA box X[NP][C][IPTB]
   static constexpr int SLICE_P = dgr_slice_p(C);
   static constexpr int S_FLOATS = SLICE_P * C * DGR_SST;
-  static constexpr int STAGE_BYTES = 4 * (W_STAGE_FLOATS + Y_STAGE_FLOATS);
-  static constexpr int NSTAGE = (4 * STAGE_BYTES + 4 * S_FLOATS + 1024 <= 220 * 1024) ? 4 : (3 * STAGE_BYTES + 4 * S_FLOATS + 1024 <= 220 * 1024) ? 3 : 2;
-  static constexpr int SMEM_BYTES = NSTAGE * STAGE_BYTES + 4 * S_FLOATS + 1024;
+  static constexpr int STAGE_BYTES = 4 * STAGE_FLOATS;
+  static constexpr int FIXED_BYTES = 4 * (2 * RAW_FLOATS + 2 * JET_FLOATS + S_FLOATS) + 1024;
+  static constexpr int NSTAGE_FIT = (225 * 1024 - FIXED_BYTES) / STAGE_BYTES;
+  static constexpr int NSTAGE = NSTAGE_FIT > 4 ? 4 : NSTAGE_FIT;
+  static constexpr int SMEM_BYTES = NSTAGE * STAGE_BYTES + FIXED_BYTES;
   static constexpr uint32_t TMEM_COLS = tc_tmem_cols(2 * N);
   static_assert(N % 16 == 0 && N <= 256, "bad N");
   static_assert(NP % SLICE_P == 0 && (SLICE_P * C) % 8 == 0, "bad slice");
+  static_assert(NSTAGE >= 2, "shared memory budget");
 };
 constexpr int DGR_THREADS = 32 * 10;   // 4 generator warps, 4 epilogue warps, MMA warp, producer warp
 constexpr int DGR_EPI_WARP0 = 4, DGR_MMA_WARP = 8;
@@ -64,15 +73,19 @@ __global__ void k_tile_w_dgr(const float* __restrict__ W, float* __restrict__ Wt
 
 template <int NF, int NS, int M, int OT>
 __global__ void __launch_bounds__(DGR_THREADS, 1)
-    k_dgrad_tc(const float* __restrict__ X, const float* __restrict__ Ybar, const float* __restrict__ Wtiled,
-               float* __restrict__ Xbar, int64_t P, int I, int IPT, int nmt, BasisCfg bc) {
+    k_dgrad_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmY,
+               const float* __restrict__ Wtiled, float* __restrict__ Xbar, int64_t P, int I, int IPT, int nmt,
+               BasisCfg bc) {
   using Cfg = DgrCfg<NF, NS, M, OT>;
   constexpr int C = Cfg::C, NP = Cfg::NP, N = Cfg::N, O = Cfg::O, NKB = Cfg::NKB, NSTAGE = Cfg::NSTAGE;
-  constexpr int SLICE_P = Cfg::SLICE_P;
+  constexpr int SLICE_P = Cfg::SLICE_P, ACS = Cfg::ACS;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   float* smem = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  float* S = smem + NSTAGE * (Cfg::W_STAGE_FLOATS + Cfg::Y_STAGE_FLOATS);
+  float* raw = smem + NSTAGE * Cfg::STAGE_FLOATS;            // [2][NP][C][KB]   Ybar boxes
+  float* jets = raw + 2 * Cfg::RAW_FLOATS;                    // [2][NP][C][IPTB] input-jet boxes
+  float* S = jets + 2 * Cfg::JET_FLOATS;                      // epilogue slice [SLICE_P*C][DGR_SST]
   __shared__ __align__(8) uint64_t full_bar[NSTAGE], empty_bar[NSTAGE], acc_full[2], acc_empty[2];
+  __shared__ __align__(8) uint64_t raw_full[2], raw_empty[2], jet_full[2], jet_empty[2];
   __shared__ uint32_t tmem_base_sh;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t p0 = (int64_t)blockIdx.x * NP;
@@ -86,6 +99,10 @@ __global__ void __launch_bounds__(DGR_THREADS, 1)
     for (int a = 0; a < 2; ++a) {
       tc::mbar_init(&acc_full[a], 1);
       tc::mbar_init(&acc_empty[a], 128);
+      tc::mbar_init(&raw_full[a], 1);
+      tc::mbar_init(&raw_empty[a], 4);     // one elected lane per generator warp
+      tc::mbar_init(&jet_full[a], 1);
+      tc::mbar_init(&jet_empty[a], 4);     // one elected lane per epilogue warp
     }
     tc::fence_mbar_init();
   }
@@ -96,54 +113,44 @@ __global__ void __launch_bounds__(DGR_THREADS, 1)
   const uint32_t tmem = tmem_base_sh;
 
   if (warp < 4) {
-    // ===================== generators: Ybar tile [N rows (p,c)][KB o] hi/lo, rows p*C + c
+    // ===================== generators: TMA'd Ybar box -> split hi/lo -> operand [KB/4][N rows][4]
+    // task = (row, chunk j), chunk fastest: conflict-free float4 reads of the box and float4 writes
+    // of the padded operand.
     constexpr int NTASK = N * (TC_KB / 4);
     constexpr int TPT = (NTASK + TC_GEN_THREADS - 1) / TC_GEN_THREADS;
     const int tid = threadIdx.x;
-    float4 buf[3][TPT];
-    auto prefetch = [&](int g, auto SLOT) {
-      constexpr int sl = decltype(SLOT)::value;
-      const int kb = g % NKB;
+    const int j = tid & 3;
+    for (int g = 0; g < nblk; ++g) {
+      const int rs = g & 1;
+      tc::mbar_wait(&raw_full[rs], (uint32_t)((g >> 1) & 1));
+      float4 v[TPT];
 #pragma unroll
       for (int u = 0; u < TPT; ++u) {
         const int task = tid + u * TC_GEN_THREADS;
-        const int row = task % N, j = task / N;
-        const int pl = row / C, c = row - pl * C;
-        const int64_t p = p0 + pl;
-        buf[sl][u] = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (task < NTASK && p < P && g < nblk)
-          buf[sl][u] = __ldg(reinterpret_cast<const float4*>(Ybar + (p * C + c) * (int64_t)O + kb * TC_KB + 4 * j));
+        v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (task < NTASK) v[u] = *reinterpret_cast<const float4*>(raw + rs * Cfg::RAW_FLOATS + (task >> 2) * TC_KB + 4 * j);
       }
-    };
-    auto step = [&](int g, auto SLOT) {
-      constexpr int sl = decltype(SLOT)::value;
-      prefetch(g + 2, std::integral_constant<int, (sl + 2) % 3>{});   // two blocks ahead
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&raw_empty[rs]);
       const int s = g % NSTAGE;
       tc::mbar_wait(&empty_bar[s], ((g / NSTAGE) & 1) ^ 1);
-      float* y_hi = smem + s * (Cfg::W_STAGE_FLOATS + Cfg::Y_STAGE_FLOATS) + Cfg::W_STAGE_FLOATS;
-      float* y_lo = y_hi + N * TC_KB;
+      float* y_hi = smem + s * Cfg::STAGE_FLOATS + Cfg::W_STAGE_FLOATS;
+      float* y_lo = y_hi + (TC_KB / 4) * ACS;
 #pragma unroll
       for (int u = 0; u < TPT; ++u) {
         const int task = tid + u * TC_GEN_THREADS;
         if (task >= NTASK) break;
-        const int row = task % N, j = task / N;
+        const int row = task >> 2;
         float4 h, l;
-        tc::split_tf32(buf[sl][u].x, h.x, l.x);
-        tc::split_tf32(buf[sl][u].y, h.y, l.y);
-        tc::split_tf32(buf[sl][u].z, h.z, l.z);
-        tc::split_tf32(buf[sl][u].w, h.w, l.w);
-        *reinterpret_cast<float4*>(y_hi + (j * N + row) * 4) = h;
-        *reinterpret_cast<float4*>(y_lo + (j * N + row) * 4) = l;
+        tc::split_tf32(v[u].x, h.x, l.x);
+        tc::split_tf32(v[u].y, h.y, l.y);
+        tc::split_tf32(v[u].z, h.z, l.z);
+        tc::split_tf32(v[u].w, h.w, l.w);
+        *reinterpret_cast<float4*>(y_hi + j * ACS + row * 4) = h;
+        *reinterpret_cast<float4*>(y_lo + j * ACS + row * 4) = l;
       }
       tc::fence_proxy_async_smem();
       tc::mbar_arrive(&full_bar[s]);
-    };
-    prefetch(0, std::integral_constant<int, 0>{});
-    prefetch(1, std::integral_constant<int, 1>{});
-    for (int g = 0; g < nblk; g += 3) {
-      step(g, std::integral_constant<int, 0>{});
-      if (g + 1 < nblk) step(g + 1, std::integral_constant<int, 1>{});
-      if (g + 2 < nblk) step(g + 2, std::integral_constant<int, 2>{});
     }
   } else if (warp < DGR_MMA_WARP) {
     // ===================== epilogue: per M-tile, TMEM -> smem slices -> jet-chain gather
@@ -154,6 +161,8 @@ __global__ void __launch_bounds__(DGR_THREADS, 1)
       const int buf = mt & 1;
       tc::mbar_wait(&acc_full[buf], (uint32_t)((mt >> 1) & 1));
       tc::tc_fence_after();
+      tc::mbar_wait(&jet_full[buf], (uint32_t)((mt >> 1) & 1));
+      const float* js = jets + buf * Cfg::JET_FLOATS + ((mt * IPT) & 3);   // [NP][C][IPTB] from input (mt*IPT) & ~3
       const int n_in = min(IPT, I - mt * IPT);    // inputs in this tile
 #pragma unroll 1
       for (int sl = 0; sl < NP / SLICE_P; ++sl) {
@@ -170,13 +179,20 @@ __global__ void __launch_bounds__(DGR_THREADS, 1)
           tc::mbar_arrive(&acc_empty[buf]);
         }
         tc::named_bar_sync(1, 128);
+        // task = (point pq, input il), input fastest: Xbar stores run along i
         for (int task = etid; task < SLICE_P * n_in; task += 128) {
-          const int pq = task % SLICE_P, il = task / SLICE_P;
-          const int64_t p = p0 + sl * SLICE_P + pq;
+          const int il = task % n_in, pq = task / n_in;
+          const int pl = sl * SLICE_P + pq;
+          const int64_t p = p0 + pl;
           const int i = mt * IPT + il;
           if (p >= P) continue;
-          float x, dx[NF > 0 ? NF : 1], ddx[NS > 0 ? NS : 1];
-          load_jet<NF, NS, false>(X, p, i, I, x, dx, ddx);
+          const float* jq = js + (pl * C) * DGR_IPTB + il;
+          const float x = jq[0];
+          float dx[NF > 0 ? NF : 1], ddx[NS > 0 ? NS : 1];
+#pragma unroll
+          for (int a = 0; a < NF; ++a) dx[a] = jq[(1 + a) * DGR_IPTB];
+#pragma unroll
+          for (int a = 0; a < NS; ++a) ddx[a] = jq[(1 + NF + a) * DGR_IPTB];
           const int n0 = first_basis(x, bc);
           float xb = 0.f, dxb[NF > 0 ? NF : 1], ddxb[NS > 0 ? NS : 1];
 #pragma unroll
@@ -217,6 +233,8 @@ __global__ void __launch_bounds__(DGR_THREADS, 1)
         }
         tc::named_bar_sync(1, 128);
       }
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&jet_empty[buf]);
     }
   } else if (warp == DGR_MMA_WARP) {
     if (lane == 0) {
@@ -231,16 +249,16 @@ __global__ void __launch_bounds__(DGR_THREADS, 1)
           const int g = mt * NKB + kb, s = g % NSTAGE;
           tc::mbar_wait(&full_bar[s], (g / NSTAGE) & 1);
           tc::tc_fence_after();
-          const float* w_hi = smem + s * (Cfg::W_STAGE_FLOATS + Cfg::Y_STAGE_FLOATS);
+          const float* w_hi = smem + s * Cfg::STAGE_FLOATS;
           const float* w_lo = w_hi + 128 * TC_KB;
           const float* y_hi = w_hi + Cfg::W_STAGE_FLOATS;
-          const float* y_lo = y_hi + N * TC_KB;
+          const float* y_lo = y_hi + (TC_KB / 4) * ACS;
 #pragma unroll
           for (int ks = 0; ks < TC_KB / 8; ++ks) {
             const uint64_t wh = tc::smem_desc(tc::smem_u32(w_hi) + 2 * ks * 128 * 16, 128 * 16, 128);
             const uint64_t wl = tc::smem_desc(tc::smem_u32(w_lo) + 2 * ks * 128 * 16, 128 * 16, 128);
-            const uint64_t yh = tc::smem_desc(tc::smem_u32(y_hi) + 2 * ks * N * 16, N * 16, 128);
-            const uint64_t yl = tc::smem_desc(tc::smem_u32(y_lo) + 2 * ks * N * 16, N * 16, 128);
+            const uint64_t yh = tc::smem_desc(tc::smem_u32(y_hi) + 2 * ks * ACS * 4, ACS * 4, 128);
+            const uint64_t yl = tc::smem_desc(tc::smem_u32(y_lo) + 2 * ks * ACS * 4, ACS * 4, 128);
             const uint32_t d = tmem + (uint32_t)(buf * N);
             tc::mma_tf32(d, wl, yh, idesc, (kb > 0 || ks > 0) ? 1u : 0u);
             tc::mma_tf32(d, wh, yl, idesc, 1u);
@@ -253,14 +271,27 @@ __global__ void __launch_bounds__(DGR_THREADS, 1)
     }
     __syncwarp();
   } else {
-    // ===================== bulk-copy producer of the pre-tiled W^T hi/lo stage
+    // ===================== producer: Ybar boxes (TMA), W^T stages (bulk copy), input-jet boxes (TMA)
     if (lane == 0) {
+      tc::tma_prefetch_desc(&tmX);
+      tc::tma_prefetch_desc(&tmY);
       for (int g = 0; g < nblk; ++g) {
+        const int mt = g / NKB, kb = g - (g / NKB) * NKB;
+        const int rs = g & 1;
+        if (g >= 2) tc::mbar_wait(&raw_empty[rs], (uint32_t)(((g >> 1) - 1) & 1));
+        tc::mbar_arrive_expect_tx(&raw_full[rs], Cfg::RAW_FLOATS * 4);
+        tc::tma_load_3d(raw + rs * Cfg::RAW_FLOATS, &tmY, kb * TC_KB, 0, (int)p0, &raw_full[rs]);
+        if (kb == 0) {
+          const int jb = mt & 1;
+          if (mt >= 2) tc::mbar_wait(&jet_empty[jb], (uint32_t)(((mt >> 1) - 1) & 1));
+          tc::mbar_arrive_expect_tx(&jet_full[jb], Cfg::JET_FLOATS * 4);
+          tc::tma_load_3d(jets + jb * Cfg::JET_FLOATS, &tmX, (mt * IPT) & ~3, 0, (int)p0, &jet_full[jb]);
+        }
         const int s = g % NSTAGE;
         tc::mbar_wait(&empty_bar[s], ((g / NSTAGE) & 1) ^ 1);
         tc::mbar_arrive_expect_tx(&full_bar[s], Cfg::W_STAGE_FLOATS * 4);
-        tc::bulk_g2s(smem + s * (Cfg::W_STAGE_FLOATS + Cfg::Y_STAGE_FLOATS), Wtiled + (int64_t)g * Cfg::W_STAGE_FLOATS,
-                     Cfg::W_STAGE_FLOATS * 4, &full_bar[s]);
+        tc::bulk_g2s(smem + s * Cfg::STAGE_FLOATS, Wtiled + (int64_t)g * Cfg::W_STAGE_FLOATS, Cfg::W_STAGE_FLOATS * 4,
+                     &full_bar[s]);
       }
     }
     __syncwarp();

@@ -493,10 +493,14 @@ hrkan_status launch_dgrad_tc(hrkan_net* net, int l, const float* X, const float*
     attr_set = true;
   }
   const TcLayerState& ls = net->tc_layers[l];
+  const int I = net->widths[l];
+  CUtensorMap tmX, tmY;
+  HR_TRY(make_tmap_f32_3d(&tmX, X, (uint64_t)I, (uint64_t)Cfg::C, (uint64_t)n, DGR_IPTB, Cfg::C, Cfg::NP));
+  HR_TRY(make_tmap_f32_3d(&tmY, Ybar, (uint64_t)Cfg::O, (uint64_t)Cfg::C, (uint64_t)n, TC_KB, Cfg::C, Cfg::NP));
   const unsigned grid = (unsigned)((n + Cfg::NP - 1) / Cfg::NP);
   HR_LAUNCH(HRKAN_K_DGRAD_HIDDEN, "k_dgrad_tc",
-            kfn<<<grid, DGR_THREADS, Cfg::SMEM_BYTES, st>>>(X, Ybar, ls.w_dgr, Xbar, n, net->widths[l], 128 / net->B,
-                                                            ls.ntile_dgr, net->bc));
+            kfn<<<grid, DGR_THREADS, Cfg::SMEM_BYTES, st>>>(tmX, tmY, ls.w_dgr, Xbar, n, I, 128 / net->B, ls.ntile_dgr,
+                                                            net->bc));
   return HRKAN_OK;
 }
 
@@ -509,6 +513,7 @@ hrkan_status tc_dgrad_layer(hrkan_net* net, int l, const float* X, const float* 
     return HRKAN_OK;
   } else {
     if (!tc_layer_ok(net, l) || l >= (int)net->tc_layers.size() || !net->tc_layers[l].w_dgr) return HRKAN_OK;
+    if (128 / net->B + 3 > DGR_IPTB) return HRKAN_OK;   // input-aligned M-tile wider than the jet box
     const int O = net->widths[l + 1];
     if (O == 128) HR_TRY(launch_dgrad_tc<NF, NS, M, 1>(net, l, X, Ybar, Xbar, n, st));
     else HR_TRY(launch_dgrad_tc<NF, NS, M, 2>(net, l, X, Ybar, Xbar, n, st));
