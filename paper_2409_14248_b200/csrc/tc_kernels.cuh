@@ -452,14 +452,17 @@ hrkan_status launch_wgrad_tc(hrkan_net* net, int l, const float* X, const float*
   int nslab = (int)std::max<int64_t>(1, (4 * net->num_sms + nmt / 2) / nmt);
   nslab = (int)std::min<int64_t>(nslab, std::max<int64_t>(1, n / 64));
   int64_t slab = (n + nslab - 1) / nslab;
-  slab = (slab + 7) / 8 * 8;
+  slab = (slab + WGR_JP - 1) / WGR_JP * WGR_JP;       // jet boxes of 32 points never straddle slabs
   nslab = (int)((n + slab - 1) / slab);
   const size_t part_bytes = sizeof(float) * ((size_t)nslab * O * K + (size_t)64 * O);
   HR_CUDA(net->tc_ws.ensure(part_bytes));
   float* part = net->tc_ws.f();
   float* part_b = part + (size_t)nslab * O * K;
+  CUtensorMap tmX, tmY;
+  HR_TRY(make_tmap_f32_3d(&tmX, X, (uint64_t)I, (uint64_t)C, (uint64_t)n, WGR_IW, C, WGR_JP));
+  HR_TRY(make_tmap_f32_3d(&tmY, Ybar, (uint64_t)O, (uint64_t)C, (uint64_t)n, O, 1, 8));
   HR_LAUNCH(HRKAN_K_WGRAD_HIDDEN, "k_wgrad_tc",
-            kfn<<<(unsigned)(nslab * nmt), WGR_THREADS, Cfg::SMEM_BYTES, st>>>(X, Ybar, part, n, I, nmt, slab,
+            kfn<<<(unsigned)(nslab * nmt), WGR_THREADS, Cfg::SMEM_BYTES, st>>>(tmX, tmY, part, n, I, nmt, slab,
                                                                                net->tc_wseg, net->bc));
   HR_LAUNCH(HRKAN_K_REDUCE, "k_reduce_slabs",
             k_reduce_slabs<<<(unsigned)((O * K + 255) / 256), 256, 0, st>>>(part, nslab, (int64_t)O * K, dW));
