@@ -72,6 +72,13 @@ def class_flops(w: HI.Workload, n_int: int, n_bi: int, c_int: int):
     return out
 
 
+def tensor_core_layers(w: HI.Workload, engine: int) -> bool:
+    """True when the hidden layers run on the tcgen05 kernels (libhrkan's tc_layer_ok rule)."""
+    hidden = [(w.widths[l], w.widths[l + 1]) for l in range(1, len(w.widths) - 2)]
+    return engine != 1 and bool(hidden) and all(O in (128, 256) and I % 8 == 0 and
+                                                (engine == 2 or I * w.B >= 256) and w.B >= 8 for I, O in hidden)
+
+
 def interior_channels(w: HI.Workload) -> int:
     return 1 + 2 + 1 if w.pde == "burgers" else 1 + 2 * w.D
 
@@ -366,10 +373,9 @@ def main():
     n_sms = torch.cuda.get_device_properties(dev).multi_processor_count
     fp32_peak = n_sms * 128 * 2 * clock_mhz * 1e6 / 1e12
     tf32_peak = pk["bf16_sustained"] * (1.1 / 2.25)
-    engine = os.environ.get("HRKAN_ROOFLINE_BOUND", "alu")
     achieved = dom_flops / (dom_ms / 1000.0) / 1e12 if dom_ms > 0 else 0.0
-    if engine == "tensor":
-        peak, bound = tf32_peak, "tensor"
+    if dominant in ("fwd_hidden", "wgrad_hidden", "dgrad_hidden") and tensor_core_layers(w, args.engine):
+        peak, bound = tf32_peak, "tensor"      # 3xTF32 tcgen05 kernels: TF32 tensor peak
     else:
         peak, bound = fp32_peak, "alu"
     roofline = {"kernel_class": dominant, "bound": bound, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
@@ -377,7 +383,9 @@ def main():
                 "launches": dom_n, "avg_launch_ms": dom_ms / max(1, dom_n), "share_of_step": share,
                 "algorithmic_flops_per_step": fl.get(dominant, 0),
                 "peak_note": (f"FP32 FFMA = {n_sms} SMs x 128 lanes x 2 x {clock_mhz:.0f} MHz (derived)" if bound == "alu"
-                              else f"TF32 = bf16 sustained {pk['bf16_sustained']} x 1.1/2.25 ({pk['source']})"),
+                              else f"TF32 dense = measured bf16 sustained {pk['bf16_sustained']} TFLOP/s x 1.1/2.25 "
+                                   f"(guide's nominal TF32/BF16 ratio; {pk['source']}); 3xTF32 issues 3 MMAs per "
+                                   f"product, so frac <= 1/3"),
                 "per_class_ms_per_step": {k: v[0] / args.steps for k, v in prof.items() if v[1]}}
 
     if rank == 0:

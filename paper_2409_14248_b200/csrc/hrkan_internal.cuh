@@ -118,7 +118,7 @@ struct hrkan_net {
   int64_t launches = 0;
   int num_sms = 148;
   // workspace
-  DevBuf jets, adj_a, adj_b, loss_part, w_part, b_part, last_part;
+  DevBuf jets, adj_a, adj_b, loss_part, w_part, b_part, last_part, first_part;
   DevBuf st_int, st_f, st_bnd, st_gb, st_ini, st_gi, st_out, st_pts, st_u, st_du, st_d2u;
   DevBuf tc_ws;                         // tensor-core path scratch
   std::vector<TcLayerState> tc_layers;

@@ -5,6 +5,7 @@
 #include "hrkan_internal.cuh"
 #include "simt_kernels.cuh"
 #include "last_kernels.cuh"
+#include "first_kernels.cuh"
 #include "tc_kernels.cuh"
 
 namespace {
@@ -76,9 +77,11 @@ hrkan_status run_pass(hrkan_net* net, const PassArgs& a, cudaStream_t st) {
         const int64_t tot = n * O;
         const unsigned grid = (unsigned)((tot + 255) / 256);
         const int cls = (l == 0) ? HRKAN_K_FWD_FIRST : HRKAN_K_FWD_HIDDEN;
-        if (l == 0)
-          HR_LAUNCH(cls, "k_fwd_simt", k_fwd_simt<NF, NS, M, true><<<grid, 256, 0, st>>>(in, net->wt[l], net->params + net->b_off[l], jet[l + 1], n, I, O, bc));
-        else
+        if (l == 0) {
+          const int bd = std::min(FL_THREADS, (O + 31) / 32 * 32);
+          const unsigned gf = (unsigned)std::min<int64_t>((n + FL_BATCH - 1) / FL_BATCH, 16 * net->num_sms);
+          HR_LAUNCH(cls, "k_fwd_first", k_fwd_first<NF, NS, M><<<gf, bd, 0, st>>>(in, net->wt[l], net->params + net->b_off[l], jet[l + 1], n, I, O, bc));
+        } else
           HR_LAUNCH(cls, "k_fwd_simt", k_fwd_simt<NF, NS, M, false><<<grid, 256, 0, st>>>(in, net->wt[l], net->params + net->b_off[l], jet[l + 1], n, I, O, bc));
       }
     }
@@ -128,9 +131,21 @@ hrkan_status run_pass(hrkan_net* net, const PassArgs& a, cudaStream_t st) {
         const size_t smem = sizeof(float) * WG_I * net->B * WG_J;
         const int cls = (l == 0) ? HRKAN_K_WGRAD_FIRST : HRKAN_K_WGRAD_HIDDEN;
         if (l == 0) {
-          auto kfn = k_wgrad_simt<NF, NS, M, true>;
-          if (smem > 48 * 1024) HR_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-          HR_LAUNCH(cls, "k_wgrad_simt", kfn<<<grid, blk, smem, st>>>(in, ybar, net->w_part.f(), net->b_part.f(), n, I, O, bc));
+          // first layer: batched shared basis tables, one thread per output neuron
+          auto kfn = k_wgrad_first<NF, NS, M>;
+          const size_t fsm = sizeof(float) * (size_t)I * net->B * O;
+          if (fsm > 200 * 1024 || O > 2 * FL_THREADS) return fail(HRKAN_EUNSUPPORTED, "first layer too wide");
+          if (fsm > 48 * 1024) HR_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm));
+          const int bd = std::min(FL_THREADS, (O + 31) / 32 * 32);
+          const int nzf = (int)std::max<int64_t>(1, std::min<int64_t>(2 * net->num_sms, n / 64));
+          const int64_t nWf = (int64_t)O * I * net->B;
+          HR_CUDA(net->first_part.ensure(sizeof(float) * (size_t)nzf * (nWf + O)));
+          float* fpart = net->first_part.f();
+          float* fpart_b = fpart + (size_t)nzf * nWf;
+          HR_LAUNCH(cls, "k_wgrad_first", kfn<<<nzf, bd, fsm, st>>>(in, ybar, fpart, fpart_b, n, I, O, bc));
+          HR_LAUNCH(HRKAN_K_REDUCE, "k_reduce_parts",
+                    k_reduce_parts<<<(unsigned)((nWf + O + 255) / 256), 256, 0, st>>>(fpart, fpart_b, nzf, nWf, O, dW, db));
+          continue;
         } else {
           auto kfn = k_wgrad_simt<NF, NS, M, false>;
           if (smem > 48 * 1024) HR_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

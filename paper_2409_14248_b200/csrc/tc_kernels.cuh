@@ -454,7 +454,7 @@ hrkan_status launch_wgrad_tc(hrkan_net* net, int l, const float* X, const float*
   int64_t slab = (n + nslab - 1) / nslab;
   slab = (slab + WGR_JP - 1) / WGR_JP * WGR_JP;       // jet boxes of 32 points never straddle slabs
   nslab = (int)((n + slab - 1) / slab);
-  const size_t part_bytes = sizeof(float) * ((size_t)nslab * O * K + (size_t)64 * O);
+  const size_t part_bytes = sizeof(float) * ((size_t)nslab * O * K + (size_t)1024 * O);
   HR_CUDA(net->tc_ws.ensure(part_bytes));
   float* part = net->tc_ws.f();
   float* part_b = part + (size_t)nslab * O * K;
@@ -466,7 +466,7 @@ hrkan_status launch_wgrad_tc(hrkan_net* net, int l, const float* X, const float*
                                                                                net->tc_wseg, net->bc));
   HR_LAUNCH(HRKAN_K_REDUCE, "k_reduce_slabs",
             k_reduce_slabs<<<(unsigned)((O * K + 255) / 256), 256, 0, st>>>(part, nslab, (int64_t)O * K, dW));
-  const int nz = (int)std::min<int64_t>(64, std::max<int64_t>(1, n / 256));
+  const int nz = (int)std::min<int64_t>(1024, std::max<int64_t>(1, n / 256));
   HR_LAUNCH(HRKAN_K_REDUCE, "k_bias_part",
             k_bias_part<<<dim3((O + 127) / 128, nz), 128, 0, st>>>(Ybar, C, O, n, part_b));
   HR_LAUNCH(HRKAN_K_REDUCE, "k_reduce_bias", k_reduce_bias<<<(O + 127) / 128, 128, 0, st>>>(part_b, nz, O, db));
