@@ -87,8 +87,8 @@ struct DevBuf {
 
 // Per-layer state of the tensor-core engine (tc_kernels.cuh).
 struct TcLayerState {
-  float* w_fwd = nullptr;   // pre-tiled, pre-split W for the forward kernel
-  float* w_dgr = nullptr;   // pre-tiled, pre-split W^T for the dgrad kernel
+  uint16_t* w_fwd = nullptr;   // pre-tiled, bf16 hi/lo-split W for the forward kernel
+  uint16_t* w_dgr = nullptr;   // pre-tiled, bf16 hi/lo-split W^T for the dgrad kernel
   int nkb = 0;              // forward K-blocks
   int ntile_dgr = 0;        // dgrad M-tiles
 };

@@ -1,7 +1,7 @@
 // tc_dgrad.cuh -- tensor-core input-adjoint kernel of a hidden layer, included by
 // tc_kernels.cuh.
 //
-//   Abar^c[p,(i,n)] = sum_o Ybar^c[p,o] W[o,(i,n)]                  (3xTF32 tcgen05, fp32 TMEM)
+//   Abar^c[p,(i,n)] = sum_o Ybar^c[p,o] W[o,(i,n)]                  (bf16x3 tcgen05, fp32 TMEM)
 // then the jet-chain epilogue (v1, v2, v3 = first/second/third x-derivatives of basis n at x_i):
 //   xbar    = sum_n [Abar^0 v1 + sum_a Abar^{1,a} v2 dx_a + sum_a Abar^{2,a} (v3 dx_a^2 + v2 ddx_a)]
 //   dxbar_a = sum_n [Abar^{1,a} v1 + 2 Abar^{2,a} v2 dx_a],     ddxbar_a = sum_n Abar^{2,a} v1
@@ -28,60 +28,60 @@ struct DgrCfg {
   static constexpr int N = NP * C;
   static constexpr int O = 128 * OT;
   static constexpr int NKB = O / TC_KB;
-  static constexpr int ACS = N * 4 + 8;                       // padded chunk stride of the Ybar operand
-  static constexpr int W_STAGE_FLOATS = 2 * 128 * TC_KB;
-  static constexpr int Y_STAGE_FLOATS = 2 * (TC_KB / 4) * ACS;
-  static constexpr int STAGE_FLOATS = W_STAGE_FLOATS + Y_STAGE_FLOATS;
+  static constexpr int ACSB = N * 16 + 64;                    // padded chunk stride of the Ybar operand (bytes)
+  static constexpr int W_STAGE_BYTES = 2 * 2 * 128 * 16;      // W^T hi + lo, [2 chunks][128 rows][8] bf16
+  static constexpr int Y_STAGE_BYTES = 2 * 2 * ACSB;          // Ybar hi + lo, [2 chunks][N rows][8] bf16
+  static constexpr int STAGE_BYTES = W_STAGE_BYTES + Y_STAGE_BYTES;
   static constexpr int RAW_FLOATS = N * TC_KB;                // TMA box Ybar[NP][C][KB]
   static constexpr int JET_FLOATS = N * DGR_IPTB;             // TMA box X[NP][C][IPTB]
   static constexpr int SLICE_P = dgr_slice_p(C);
   static constexpr int S_FLOATS = SLICE_P * C * DGR_SST;
-  static constexpr int STAGE_BYTES = 4 * STAGE_FLOATS;
   static constexpr int FIXED_BYTES = 4 * (2 * RAW_FLOATS + 2 * JET_FLOATS + S_FLOATS) + 1024;
   static constexpr int NSTAGE_FIT = (225 * 1024 - FIXED_BYTES) / STAGE_BYTES;
-  static constexpr int NSTAGE = NSTAGE_FIT > 4 ? 4 : NSTAGE_FIT;
+  static constexpr int NSTAGE = NSTAGE_FIT > 6 ? 6 : NSTAGE_FIT;
   static constexpr int SMEM_BYTES = NSTAGE * STAGE_BYTES + FIXED_BYTES;
   static constexpr uint32_t TMEM_COLS = tc_tmem_cols(2 * N);
   static_assert(N % 16 == 0 && N <= 256, "bad N");
   static_assert(NP % SLICE_P == 0 && (SLICE_P * C) % 8 == 0, "bad slice");
   static_assert(NSTAGE >= 2, "shared memory budget");
+  static_assert(STAGE_BYTES % 128 == 0, "TMA boxes after the stages need 128-B alignment");
 };
 constexpr int DGR_THREADS = 32 * 10;   // 4 generator warps, 4 epilogue warps, MMA warp, producer warp
 constexpr int DGR_EPI_WARP0 = 4, DGR_MMA_WARP = 8;
 
 // W^T tiles for k_dgrad_tc: for M-tile mt (inputs mt*IPT ...), K-block kb (o = kb*KB ...):
-// [hi | lo] each [KB/4][128 rows][4], row = il*B + n (il < IPT), zero outside.
-__global__ void k_tile_w_dgr(const float* __restrict__ W, float* __restrict__ Wt, int O, int I, int B, int IPT,
+// [hi | lo] each [2 chunks][128 rows][8] bf16, row = il*B + n (il < IPT), zero outside.
+__global__ void k_tile_w_dgr(const float* __restrict__ W, uint16_t* __restrict__ Wt, int O, int I, int B, int IPT,
                              int nmt) {
   const int nkb = O / TC_KB;
   const int64_t per = 128 * TC_KB;
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t >= per * nkb * nmt) return;
   const int64_t blk = t / per;
-  const int r4 = (int)(t - blk * per);             // (j*128 + row)*4 + e
+  const int r8 = (int)(t - blk * per);             // (ch*128 + row)*8 + e
   const int mt = (int)(blk / nkb), kb = (int)(blk - (int64_t)mt * nkb);
-  const int e = r4 & 3, row = (r4 >> 2) & 127, j = r4 >> 9;
-  const int o = kb * TC_KB + 4 * j + e;
+  const int e = r8 & 7, row = (r8 >> 3) & 127, ch = r8 >> 10;
+  const int o = kb * TC_KB + 8 * ch + e;
   const int il = row / B, n = row - il * B, i = mt * IPT + il;
   const float w = (il < IPT && i < I) ? W[((int64_t)o * I + i) * B + n] : 0.f;
-  float hi, lo;
-  tc::split_tf32(w, hi, lo);
-  float* dst = Wt + blk * 2 * per;
-  dst[r4] = hi;
-  dst[per + r4] = lo;
+  uint16_t hi, lo;
+  tc::split1_bf16(w, hi, lo);
+  uint16_t* dst = Wt + blk * 2 * per;
+  dst[r8] = hi;
+  dst[per + r8] = lo;
 }
 
 template <int NF, int NS, int M, int OT>
 __global__ void __launch_bounds__(DGR_THREADS, 1)
     k_dgrad_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmY,
-               const float* __restrict__ Wtiled, float* __restrict__ Xbar, int64_t P, int I, int IPT, int nmt,
+               const uint16_t* __restrict__ Wtiled, float* __restrict__ Xbar, int64_t P, int I, int IPT, int nmt,
                BasisCfg bc) {
   using Cfg = DgrCfg<NF, NS, M, OT>;
   constexpr int C = Cfg::C, NP = Cfg::NP, N = Cfg::N, O = Cfg::O, NKB = Cfg::NKB, NSTAGE = Cfg::NSTAGE;
-  constexpr int SLICE_P = Cfg::SLICE_P, ACS = Cfg::ACS;
+  constexpr int SLICE_P = Cfg::SLICE_P, ACSB = Cfg::ACSB;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  float* smem = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  float* raw = smem + NSTAGE * Cfg::STAGE_FLOATS;            // [2][NP][C][KB]   Ybar boxes
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  float* raw = reinterpret_cast<float*>(smem + NSTAGE * Cfg::STAGE_BYTES);   // [2][NP][C][KB]   Ybar boxes
   float* jets = raw + 2 * Cfg::RAW_FLOATS;                    // [2][NP][C][IPTB] input-jet boxes
   float* S = jets + 2 * Cfg::JET_FLOATS;                      // epilogue slice [SLICE_P*C][DGR_SST]
   __shared__ __align__(8) uint64_t full_bar[NSTAGE], empty_bar[NSTAGE], acc_full[2], acc_empty[2];
@@ -113,41 +113,44 @@ __global__ void __launch_bounds__(DGR_THREADS, 1)
   const uint32_t tmem = tmem_base_sh;
 
   if (warp < 4) {
-    // ===================== generators: TMA'd Ybar box -> split hi/lo -> operand [KB/4][N rows][4]
-    // task = (row, chunk j), chunk fastest: conflict-free float4 reads of the box and float4 writes
-    // of the padded operand.
-    constexpr int NTASK = N * (TC_KB / 4);
+    // ===================== generators: TMA'd Ybar box -> bf16 hi/lo -> operand [2 chunks][N rows][8]
+    // task = (row, chunk h), chunk fastest: two float4 reads of the box, one 16-B store per half,
+    // conflict-free on the padded operand.
+    constexpr int NTASK = N * 2;
     constexpr int TPT = (NTASK + TC_GEN_THREADS - 1) / TC_GEN_THREADS;
     const int tid = threadIdx.x;
-    const int j = tid & 3;
+    const int h = tid & 1;
     for (int g = 0; g < nblk; ++g) {
       const int rs = g & 1;
       tc::mbar_wait(&raw_full[rs], (uint32_t)((g >> 1) & 1));
-      float4 v[TPT];
+      float v[TPT][8];
 #pragma unroll
       for (int u = 0; u < TPT; ++u) {
         const int task = tid + u * TC_GEN_THREADS;
-        v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (task < NTASK) v[u] = *reinterpret_cast<const float4*>(raw + rs * Cfg::RAW_FLOATS + (task >> 2) * TC_KB + 4 * j);
+        float4 p = make_float4(0.f, 0.f, 0.f, 0.f), q = p;
+        if (task < NTASK) {
+          const float* src = raw + rs * Cfg::RAW_FLOATS + (task >> 1) * TC_KB + 8 * h;
+          p = *reinterpret_cast<const float4*>(src);
+          q = *reinterpret_cast<const float4*>(src + 4);
+        }
+        v[u][0] = p.x; v[u][1] = p.y; v[u][2] = p.z; v[u][3] = p.w;
+        v[u][4] = q.x; v[u][5] = q.y; v[u][6] = q.z; v[u][7] = q.w;
       }
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&raw_empty[rs]);
       const int s = g % NSTAGE;
       tc::mbar_wait(&empty_bar[s], ((g / NSTAGE) & 1) ^ 1);
-      float* y_hi = smem + s * Cfg::STAGE_FLOATS + Cfg::W_STAGE_FLOATS;
-      float* y_lo = y_hi + (TC_KB / 4) * ACS;
+      uint8_t* y_hi = smem + s * Cfg::STAGE_BYTES + Cfg::W_STAGE_BYTES;
+      uint8_t* y_lo = y_hi + 2 * ACSB;
 #pragma unroll
       for (int u = 0; u < TPT; ++u) {
         const int task = tid + u * TC_GEN_THREADS;
         if (task >= NTASK) break;
-        const int row = task >> 2;
-        float4 h, l;
-        tc::split_tf32(v[u].x, h.x, l.x);
-        tc::split_tf32(v[u].y, h.y, l.y);
-        tc::split_tf32(v[u].z, h.z, l.z);
-        tc::split_tf32(v[u].w, h.w, l.w);
-        *reinterpret_cast<float4*>(y_hi + j * ACS + row * 4) = h;
-        *reinterpret_cast<float4*>(y_lo + j * ACS + row * 4) = l;
+        const int row = task >> 1;
+        uint4 hh, ll;
+        tc::split8_bf16(v[u], hh, ll);
+        *reinterpret_cast<uint4*>(y_hi + h * ACSB + row * 16) = hh;
+        *reinterpret_cast<uint4*>(y_lo + h * ACSB + row * 16) = ll;
       }
       tc::fence_proxy_async_smem();
       tc::mbar_arrive(&full_bar[s]);
@@ -238,7 +241,7 @@ __global__ void __launch_bounds__(DGR_THREADS, 1)
     }
   } else if (warp == DGR_MMA_WARP) {
     if (lane == 0) {
-      constexpr uint32_t idesc = tc::idesc_tf32(128, N);
+      constexpr uint32_t idesc = tc::idesc_bf16(128, N);
       for (int mt = 0; mt < nmt; ++mt) {
         const int buf = mt & 1;
         if (mt >= 2) {
@@ -249,21 +252,18 @@ __global__ void __launch_bounds__(DGR_THREADS, 1)
           const int g = mt * NKB + kb, s = g % NSTAGE;
           tc::mbar_wait(&full_bar[s], (g / NSTAGE) & 1);
           tc::tc_fence_after();
-          const float* w_hi = smem + s * Cfg::STAGE_FLOATS;
-          const float* w_lo = w_hi + 128 * TC_KB;
-          const float* y_hi = w_hi + Cfg::W_STAGE_FLOATS;
-          const float* y_lo = y_hi + (TC_KB / 4) * ACS;
-#pragma unroll
-          for (int ks = 0; ks < TC_KB / 8; ++ks) {
-            const uint64_t wh = tc::smem_desc(tc::smem_u32(w_hi) + 2 * ks * 128 * 16, 128 * 16, 128);
-            const uint64_t wl = tc::smem_desc(tc::smem_u32(w_lo) + 2 * ks * 128 * 16, 128 * 16, 128);
-            const uint64_t yh = tc::smem_desc(tc::smem_u32(y_hi) + 2 * ks * ACS * 4, ACS * 4, 128);
-            const uint64_t yl = tc::smem_desc(tc::smem_u32(y_lo) + 2 * ks * ACS * 4, ACS * 4, 128);
-            const uint32_t d = tmem + (uint32_t)(buf * N);
-            tc::mma_tf32(d, wl, yh, idesc, (kb > 0 || ks > 0) ? 1u : 0u);
-            tc::mma_tf32(d, wh, yl, idesc, 1u);
-            tc::mma_tf32(d, wh, yh, idesc, 1u);
-          }
+          const uint32_t w_hi = tc::smem_u32(smem + s * Cfg::STAGE_BYTES);
+          const uint32_t w_lo = w_hi + 2 * 128 * 16;
+          const uint32_t y_hi = w_hi + Cfg::W_STAGE_BYTES;
+          const uint32_t y_lo = y_hi + 2 * ACSB;
+          const uint64_t wh = tc::smem_desc(w_hi, 128 * 16, 128);
+          const uint64_t wl = tc::smem_desc(w_lo, 128 * 16, 128);
+          const uint64_t yh = tc::smem_desc(y_hi, ACSB, 128);
+          const uint64_t yl = tc::smem_desc(y_lo, ACSB, 128);
+          const uint32_t d = tmem + (uint32_t)(buf * N);
+          tc::mma_bf16(d, wl, yh, idesc, kb > 0 ? 1u : 0u);
+          tc::mma_bf16(d, wh, yl, idesc, 1u);
+          tc::mma_bf16(d, wh, yh, idesc, 1u);
           tc::mma_commit(&empty_bar[s]);
         }
         tc::mma_commit(&acc_full[buf]);
@@ -289,8 +289,8 @@ __global__ void __launch_bounds__(DGR_THREADS, 1)
         }
         const int s = g % NSTAGE;
         tc::mbar_wait(&empty_bar[s], ((g / NSTAGE) & 1) ^ 1);
-        tc::mbar_arrive_expect_tx(&full_bar[s], Cfg::W_STAGE_FLOATS * 4);
-        tc::bulk_g2s(smem + s * Cfg::STAGE_FLOATS, Wtiled + (int64_t)g * Cfg::W_STAGE_FLOATS, Cfg::W_STAGE_FLOATS * 4,
+        tc::mbar_arrive_expect_tx(&full_bar[s], Cfg::W_STAGE_BYTES);
+        tc::bulk_g2s(smem + s * Cfg::STAGE_BYTES, Wtiled + (int64_t)g * (Cfg::W_STAGE_BYTES / 2), Cfg::W_STAGE_BYTES,
                      &full_bar[s]);
       }
     }

@@ -49,38 +49,39 @@ struct FwdCfg {
   static constexpr int NP = tc_np(C);
   static constexpr int N = NP * C;
   static constexpr int O = 128 * NMT;
-  // generated operand: [KB/4 chunks][N rows][4], chunk stride padded to 32 B (mod 128 B) so that the
-  // generators' (chunk-fastest) float4 stores are bank-conflict free
-  static constexpr int ACS = N * 4 + 8;                      // chunk stride (floats)
-  static constexpr int W_STAGE_FLOATS = 2 * O * TC_KB;       // hi + lo, [KB/4][O][4] each
-  static constexpr int A_STAGE_FLOATS = 2 * (TC_KB / 4) * ACS;
-  static constexpr int STAGE_FLOATS = W_STAGE_FLOATS + A_STAGE_FLOATS;
-  static constexpr int STAGE_BYTES = 4 * STAGE_FLOATS;
+  // bf16 operands, K-major, SWIZZLE_NONE: a K-block of 16 = 2 chunks of 8 elements (16 B per row).
+  // Generated operand chunk stride padded to 64 B (mod 128 B): the generators' 8-B stores
+  // (4 consecutive K of one row, chunk-fastest lanes) are bank-conflict free.
+  static constexpr int ACSB = N * 16 + 64;                   // chunk stride (bytes)
+  static constexpr int W_STAGE_BYTES = 2 * 2 * O * 16;       // hi + lo, [2 chunks][O rows][8] each
+  static constexpr int A_STAGE_BYTES = 2 * 2 * ACSB;         // hi + lo, [2 chunks][N rows][8] each
+  static constexpr int STAGE_BYTES = W_STAGE_BYTES + A_STAGE_BYTES;
   static constexpr int WIN_FLOATS = NP * C * TC_WIN;         // TMA box [NP points][C][TC_WIN inputs]
   static constexpr int FIXED_BYTES = 4 * TC_NWIN * WIN_FLOATS + 4 * 256 + 1024;
   static constexpr int NSTAGE_FIT = (225 * 1024 - FIXED_BYTES) / STAGE_BYTES;   // static smem + margin
-  static constexpr int NSTAGE = NSTAGE_FIT > 4 ? 4 : NSTAGE_FIT;
+  static constexpr int NSTAGE = NSTAGE_FIT > 6 ? 6 : NSTAGE_FIT;
   static constexpr int SMEM_BYTES = NSTAGE * STAGE_BYTES + FIXED_BYTES;
   static constexpr int NACC = (2 * NMT * N <= 512) ? 2 : 1;   // double-buffered accumulators if they fit
   static constexpr uint32_t TMEM_COLS = tc_tmem_cols(NACC * NMT * N);
   static_assert(N % 16 == 0 && N <= 256, "bad N");
   static_assert(NMT * N <= 512, "accumulators exceed TMEM");
   static_assert(NSTAGE >= 2, "shared memory budget");
+  static_assert(STAGE_BYTES % 128 == 0, "TMA windows after the stages need 128-B alignment");
 };
 
-// Pre-tiled, pre-split weights for k_fwd_tc: for K-block kb: [hi | lo] each [KB/4][O][4].
-__global__ void k_tile_w_fwd(const float* __restrict__ W, float* __restrict__ Wt, int O, int K, int nkb) {
+// Pre-tiled, pre-split weights for k_fwd_tc: for K-block kb: [hi | lo] each [2 chunks][O][8] bf16.
+__global__ void k_tile_w_fwd(const float* __restrict__ W, uint16_t* __restrict__ Wt, int O, int K, int nkb) {
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int64_t per_kb = (int64_t)O * TC_KB;
+  const int64_t per_kb = (int64_t)O * TC_KB;         // elements of one of hi / lo per K-block
   if (t >= per_kb * nkb) return;
   const int kb = (int)(t / per_kb);
-  const int r = (int)(t - (int64_t)kb * per_kb);     // r = (j*O + o)*4 + e
-  const int e = r & 3, o = (r >> 2) % O, j = (r >> 2) / O;
-  const int k = kb * TC_KB + 4 * j + e;
+  const int r = (int)(t - (int64_t)kb * per_kb);     // r = (chunk*O + o)*8 + e
+  const int e = r & 7, o = (r >> 3) % O, ch = (r >> 3) / O;
+  const int k = kb * TC_KB + 8 * ch + e;
   const float w = (k < K) ? W[(int64_t)o * K + k] : 0.f;
-  float hi, lo;
-  tc::split_tf32(w, hi, lo);
-  float* dst = Wt + (int64_t)kb * 2 * per_kb;
+  uint16_t hi, lo;
+  tc::split1_bf16(w, hi, lo);
+  uint16_t* dst = Wt + (int64_t)kb * 2 * per_kb;
   dst[r] = hi;
   dst[per_kb + r] = lo;
 }
@@ -93,14 +94,14 @@ __global__ void k_tile_w_fwd(const float* __restrict__ W, float* __restrict__ Wt
 //                so the generators read the jets from shared memory (coalesced, latency hidden).
 template <int NF, int NS, int M, int NMT>
 __global__ void __launch_bounds__(TC_THREADS, 1)
-    k_fwd_tc(const __grid_constant__ CUtensorMap tmX, const float* __restrict__ Wtiled, const float* __restrict__ bias,
+    k_fwd_tc(const __grid_constant__ CUtensorMap tmX, const uint16_t* __restrict__ Wtiled, const float* __restrict__ bias,
              float* __restrict__ Y, int64_t P, int I, int nkb, int seg, BasisCfg bc) {
   using Cfg = FwdCfg<NF, NS, M, NMT>;
   constexpr int C = Cfg::C, NP = Cfg::NP, N = Cfg::N, O = Cfg::O, NACC = Cfg::NACC, NSTAGE = Cfg::NSTAGE;
-  constexpr int ACS = Cfg::ACS;
+  constexpr int ACSB = Cfg::ACSB;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  float* smem = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  float* win = smem + NSTAGE * Cfg::STAGE_FLOATS;            // [TC_NWIN][NP][C][TC_WIN]
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  float* win = reinterpret_cast<float*>(smem + NSTAGE * Cfg::STAGE_BYTES);   // [TC_NWIN][NP][C][TC_WIN]
   float* ctr = win + TC_NWIN * Cfg::WIN_FLOATS;              // basis centres mid_n, n < B
   __shared__ __align__(8) uint64_t full_bar[NSTAGE], empty_bar[NSTAGE], acc_full[NACC], acc_empty[NACC];
   __shared__ __align__(8) uint64_t win_full[TC_NWIN], win_empty[TC_NWIN];
@@ -215,8 +216,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       }
       const int s = kb % NSTAGE;
       tc::mbar_wait(&empty_bar[s], ((kb / NSTAGE) & 1) ^ 1);
-      float* a_hi = smem + s * Cfg::STAGE_FLOATS + Cfg::W_STAGE_FLOATS;
-      float* a_lo = a_hi + (TC_KB / 4) * ACS;
+      uint8_t* a_hi = smem + s * Cfg::STAGE_BYTES + Cfg::W_STAGE_BYTES;
+      uint8_t* a_lo = a_hi + 2 * ACSB;
+      const int aoff = (j >> 1) * ACSB + (j & 1) * 8;    // chunk j/2, half j%2 of the 16-B row
 #pragma unroll
       for (int u = 0; u < TPT; ++u) {
         const int task = gtid + u * TC_GEN_THREADS;
@@ -227,7 +229,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int i = i0 + h;
-          const float* wp = win + ((i >> 3) % TC_NWIN) * Cfg::WIN_FLOATS + (pl * C) * TC_WIN + (i & 7);
+          const float* wp = win + ((i / TC_WIN) % TC_NWIN) * Cfg::WIN_FLOATS + (pl * C) * TC_WIN + (i % TC_WIN);
           jx[h] = wp[0];
 #pragma unroll
           for (int a = 0; a < NF; ++a) jdx[h][a] = wp[(1 + a) * TC_WIN];
@@ -256,14 +258,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         }
 #pragma unroll
         for (int c = 0; c < C; ++c) {
-          float4 hh, ll;
-          tc::split_tf32(va[c][0], hh.x, ll.x);
-          tc::split_tf32(va[c][1], hh.y, ll.y);
-          tc::split_tf32(va[c][2], hh.z, ll.z);
-          tc::split_tf32(va[c][3], hh.w, ll.w);
+          uint2 hh, ll;
+          tc::split4_bf16(make_float4(va[c][0], va[c][1], va[c][2], va[c][3]), hh, ll);
           const int row = c * NP + pl;                  // channel-major columns of the MMA N
-          *reinterpret_cast<float4*>(a_hi + j * ACS + row * 4) = hh;
-          *reinterpret_cast<float4*>(a_lo + j * ACS + row * 4) = ll;
+          *reinterpret_cast<uint2*>(a_hi + aoff + row * 16) = hh;
+          *reinterpret_cast<uint2*>(a_lo + aoff + row * 16) = ll;
         }
       }
       tc::fence_proxy_async_smem();
@@ -278,7 +277,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   } else if (warp == TC_MMA_WARP) {
     // ===================== MMA issuer (one thread)
     if (lane == 0) {
-      constexpr uint32_t idesc = tc::idesc_tf32(128, N);
+      constexpr uint32_t idesc = tc::idesc_bf16(128, N);
       for (int kb = 0; kb < nkb; ++kb) {
         const int sg = kb / seg, buf = sg % NACC;
         const bool seg_first = (kb % seg) == 0;
@@ -289,27 +288,21 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         const int s = kb % NSTAGE;
         tc::mbar_wait(&full_bar[s], (kb / NSTAGE) & 1);
         tc::tc_fence_after();
-        const float* w_hi = smem + s * Cfg::STAGE_FLOATS;
-        const float* w_lo = w_hi + O * TC_KB;
-        const float* a_hi = w_hi + Cfg::W_STAGE_FLOATS;
-        const float* a_lo = a_hi + (TC_KB / 4) * ACS;
+        const uint32_t w_hi = tc::smem_u32(smem + s * Cfg::STAGE_BYTES);
+        const uint32_t w_lo = w_hi + 2 * O * 16;
+        const uint32_t a_hi = w_hi + Cfg::W_STAGE_BYTES;
+        const uint32_t a_lo = a_hi + 2 * ACSB;
+        // one K-step of 16 per stage: LBO = chunk stride, SBO = 8 rows = 128 B
+        const uint64_t bh = tc::smem_desc(a_hi, ACSB, 128);
+        const uint64_t bl = tc::smem_desc(a_lo, ACSB, 128);
 #pragma unroll
-        for (int ks = 0; ks < TC_KB / 8; ++ks) {
-          // K-step ks covers chunks 2ks, 2ks+1: LBO = chunk stride, SBO = 8 rows = 128 B
-          const uint32_t aoff = (uint32_t)(2 * ks * ACS * 4);
-          const uint64_t bh = tc::smem_desc(tc::smem_u32(a_hi) + aoff, ACS * 4, 128);
-          const uint64_t bl = tc::smem_desc(tc::smem_u32(a_lo) + aoff, ACS * 4, 128);
-#pragma unroll
-          for (int t = 0; t < NMT; ++t) {
-            const uint32_t woff = (uint32_t)(2 * ks * O * 16 + t * 128 * 16);
-            const uint64_t wh = tc::smem_desc(tc::smem_u32(w_hi) + woff, O * 16, 128);
-            const uint64_t wl = tc::smem_desc(tc::smem_u32(w_lo) + woff, O * 16, 128);
-            const uint32_t d = tmem + (uint32_t)((buf * NMT + t) * N);
-            const uint32_t acc0 = (seg_first && ks == 0) ? 0u : 1u;
-            tc::mma_tf32(d, wl, bh, idesc, acc0);
-            tc::mma_tf32(d, wh, bl, idesc, 1u);
-            tc::mma_tf32(d, wh, bh, idesc, 1u);
-          }
+        for (int t = 0; t < NMT; ++t) {
+          const uint64_t wh = tc::smem_desc(w_hi + t * 128 * 16, O * 16, 128);
+          const uint64_t wl = tc::smem_desc(w_lo + t * 128 * 16, O * 16, 128);
+          const uint32_t d = tmem + (uint32_t)((buf * NMT + t) * N);
+          tc::mma_bf16(d, wl, bh, idesc, seg_first ? 0u : 1u);
+          tc::mma_bf16(d, wh, bl, idesc, 1u);
+          tc::mma_bf16(d, wh, bh, idesc, 1u);
         }
         tc::mma_commit(&empty_bar[s]);
         if ((kb % seg) == seg - 1 || kb == nkb - 1) tc::mma_commit(&acc_full[buf]);
@@ -322,9 +315,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       for (int kb = 0; kb < nkb; ++kb) {
         const int s = kb % NSTAGE;
         tc::mbar_wait(&empty_bar[s], ((kb / NSTAGE) & 1) ^ 1);
-        float* w_dst = smem + s * Cfg::STAGE_FLOATS;
-        tc::mbar_arrive_expect_tx(&full_bar[s], Cfg::W_STAGE_FLOATS * 4);
-        tc::bulk_g2s(w_dst, Wtiled + (int64_t)kb * Cfg::W_STAGE_FLOATS, Cfg::W_STAGE_FLOATS * 4, &full_bar[s]);
+        tc::mbar_arrive_expect_tx(&full_bar[s], Cfg::W_STAGE_BYTES);
+        tc::bulk_g2s(smem + s * Cfg::STAGE_BYTES, Wtiled + (int64_t)kb * (Cfg::W_STAGE_BYTES / 2), Cfg::W_STAGE_BYTES,
+                     &full_bar[s]);
       }
     }
     __syncwarp();
@@ -378,7 +371,7 @@ hrkan_status tc_refresh_weights(hrkan_net* net, cudaStream_t st) {
     ls.nkb = (K + TC_KB - 1) / TC_KB;
     const size_t n = (size_t)ls.nkb * 2 * O * TC_KB;
     if (!ls.w_fwd) {
-      if (cudaMalloc(&ls.w_fwd, n * sizeof(float)) != cudaSuccess) return fail(HRKAN_ENOMEM, "tc weight alloc");
+      if (cudaMalloc(&ls.w_fwd, n * sizeof(uint16_t)) != cudaSuccess) return fail(HRKAN_ENOMEM, "tc weight alloc");
     }
     const int64_t tot = (int64_t)ls.nkb * O * TC_KB;
     HR_LAUNCH(HRKAN_K_OTHER, "k_tile_w_fwd",
@@ -388,7 +381,7 @@ hrkan_status tc_refresh_weights(hrkan_net* net, cudaStream_t st) {
     ls.ntile_dgr = (I + IPT - 1) / IPT;
     const size_t nd = (size_t)ls.ntile_dgr * (O / TC_KB) * 2 * 128 * TC_KB;
     if (!ls.w_dgr) {
-      if (cudaMalloc(&ls.w_dgr, nd * sizeof(float)) != cudaSuccess) return fail(HRKAN_ENOMEM, "tc weight alloc");
+      if (cudaMalloc(&ls.w_dgr, nd * sizeof(uint16_t)) != cudaSuccess) return fail(HRKAN_ENOMEM, "tc weight alloc");
     }
     const int64_t totd = (int64_t)ls.ntile_dgr * (O / TC_KB) * 128 * TC_KB;
     HR_LAUNCH(HRKAN_K_OTHER, "k_tile_w_dgr",
@@ -460,7 +453,7 @@ hrkan_status launch_wgrad_tc(hrkan_net* net, int l, const float* X, const float*
   float* part_b = part + (size_t)nslab * O * K;
   CUtensorMap tmX, tmY;
   HR_TRY(make_tmap_f32_3d(&tmX, X, (uint64_t)I, (uint64_t)C, (uint64_t)n, WGR_IW, C, WGR_JP));
-  HR_TRY(make_tmap_f32_3d(&tmY, Ybar, (uint64_t)O, (uint64_t)C, (uint64_t)n, O, 1, 8));
+  HR_TRY(make_tmap_f32_3d(&tmY, Ybar, (uint64_t)O, (uint64_t)C, (uint64_t)n, O, 2, 8));
   HR_LAUNCH(HRKAN_K_WGRAD_HIDDEN, "k_wgrad_tc",
             kfn<<<(unsigned)(nslab * nmt), WGR_THREADS, Cfg::SMEM_BYTES, st>>>(tmX, tmY, part, n, I, nmt, slab,
                                                                                net->tc_wseg, net->bc));

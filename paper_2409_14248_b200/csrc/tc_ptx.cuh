@@ -115,6 +115,25 @@ __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64
       : "memory");
 }
 
+// Instruction descriptor kind::f16 with BF16 A/B (K-major) and an F32 accumulator.
+__host__ __device__ constexpr uint32_t idesc_bf16(uint32_t M, uint32_t N) {
+  return (1u << 4)            // c_format F32
+         | (1u << 7)          // a_format BF16
+         | (1u << 10)         // b_format BF16
+         | ((N >> 3) << 17) | ((M >> 4) << 24);
+}
+
+// D[tmem] (+)= A[smem] * B[smem]^T, BF16 operands, K = 16 per instruction (single elected thread)
+__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
 // mbarrier arrives when all previously issued tcgen05.mma of this thread have completed
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
@@ -168,6 +187,38 @@ __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
 __device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
   hi = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
   lo = x - hi;
+}
+
+// bf16x3 split: x = hi + lo + r with hi = bf16_rn(x), lo = bf16_rn(x - hi),
+// |r| <= 2^-18 |x|; a*b ~ ah*bh + ah*bl + al*bh (the dropped al*bl is <= 2^-18 |ab|).
+// Pairs are packed little-endian: the element at the lower K index sits in the low 16 bits.
+__device__ __forceinline__ uint32_t pack_bf16x2(float e0, float e1) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(e1), "f"(e0));
+  return r;
+}
+__device__ __forceinline__ void split2_bf16(float e0, float e1, uint32_t& hi, uint32_t& lo) {
+  hi = pack_bf16x2(e0, e1);
+  const float r0 = e0 - __uint_as_float(hi << 16);
+  const float r1 = e1 - __uint_as_float(hi & 0xFFFF0000u);
+  lo = pack_bf16x2(r0, r1);
+}
+__device__ __forceinline__ void split4_bf16(float4 v, uint2& hi, uint2& lo) {
+  split2_bf16(v.x, v.y, hi.x, lo.x);
+  split2_bf16(v.z, v.w, hi.y, lo.y);
+}
+__device__ __forceinline__ void split8_bf16(const float (&v)[8], uint4& hi, uint4& lo) {
+  split2_bf16(v[0], v[1], hi.x, lo.x);
+  split2_bf16(v[2], v[3], hi.y, lo.y);
+  split2_bf16(v[4], v[5], hi.z, lo.z);
+  split2_bf16(v[6], v[7], hi.w, lo.w);
+}
+// host/device scalar version for weight tiling: returns the two bf16 bit patterns
+__device__ __forceinline__ void split1_bf16(float x, uint16_t& hi, uint16_t& lo) {
+  const uint32_t h = pack_bf16x2(x, 0.f);
+  hi = (uint16_t)(h & 0xFFFFu);
+  const uint32_t l = pack_bf16x2(x - __uint_as_float(h << 16), 0.f);
+  lo = (uint16_t)(l & 0xFFFFu);
 }
 
 }  // namespace tc
