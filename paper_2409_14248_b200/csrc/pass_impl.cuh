@@ -120,6 +120,7 @@ hrkan_status run_pass(hrkan_net* net, const PassArgs& a, cudaStream_t st) {
       float* dW = a.grad + net->w_off[l];
       float* db = a.grad + net->b_off[l];
       bool done = false;
+      if (l > 0) HR_TRY(tc_split_ybar<NF, NS, M>(net, l, ybar, n, st));   // bf16 hi/lo operands of both kernels
       if (l > 0) HR_TRY(tc_wgrad_layer<NF, NS, M>(net, l, in, ybar, dW, db, n, st, &done));
       if (!done) {
         const dim3 blk(WG_J, WG_I);

@@ -8,16 +8,15 @@
 //
 // Orientation: MMA M = rows (i,n) of an INPUT-ALIGNED tile (IPT = floor(128/B) whole inputs, so every
 // sum over n closes inside one tile), MMA N = (point, channel) columns p*C + c of NP points, MMA
-// K = o.  A = pre-tiled W^T hi/lo (one 1-D bulk copy per stage), B = Ybar hi/lo: the producer warp
-// TMA-loads the box Ybar[NP points][C][KB outputs] into a 2-deep ring and 4 generator warps split it
-// into the operand layout.  Two TMEM accumulators: the 4 epilogue warps drain M-tile t while the MMA
+// K = o.  A = pre-tiled W^T hi/lo and B = pre-split Ybar hi/lo (k_split_ybar), both by 1-D bulk
+// copies per stage.  Two TMEM accumulators: the 8 epilogue warps drain M-tile t while the MMA
 // runs t+1.  Epilogue: TMEM -> smem slice of SLICE_P points -> each (point, input) gathers only the
 // k+1 non-zero bases of its x (input jets TMA-loaded per M-tile) -> Xbar[p][c][i].
 #pragma once
 
 namespace {
 
-__host__ __device__ constexpr int dgr_slice_p(int C) { return C == 1 ? 64 : 8; }
+__host__ __device__ constexpr int dgr_slice_p(int C) { return C == 1 ? 64 : 16; }
 constexpr int DGR_SST = 129;   // column stride of the epilogue slice (odd: conflict-free gathers)
 constexpr int DGR_IPTB = 16;   // jet box width (inputs) >= IPT + 3 (box start aligned down to 16 B), B >= 11
 
@@ -28,26 +27,25 @@ struct DgrCfg {
   static constexpr int N = NP * C;
   static constexpr int O = 128 * OT;
   static constexpr int NKB = O / TC_KB;
-  static constexpr int ACSB = N * 16 + 64;                    // padded chunk stride of the Ybar operand (bytes)
   static constexpr int W_STAGE_BYTES = 2 * 2 * 128 * 16;      // W^T hi + lo, [2 chunks][128 rows][8] bf16
-  static constexpr int Y_STAGE_BYTES = 2 * 2 * ACSB;          // Ybar hi + lo, [2 chunks][N rows][8] bf16
+  static constexpr int Y_STAGE_BYTES = 2 * 2 * N * 16;        // Ybar hi + lo, [2 chunks][N rows][8] bf16
   static constexpr int STAGE_BYTES = W_STAGE_BYTES + Y_STAGE_BYTES;
-  static constexpr int RAW_FLOATS = N * TC_KB;                // TMA box Ybar[NP][C][KB]
   static constexpr int JET_FLOATS = N * DGR_IPTB;             // TMA box X[NP][C][IPTB]
   static constexpr int SLICE_P = dgr_slice_p(C);
   static constexpr int S_FLOATS = SLICE_P * C * DGR_SST;
-  static constexpr int FIXED_BYTES = 4 * (2 * RAW_FLOATS + 2 * JET_FLOATS + S_FLOATS) + 1024;
+  static constexpr int FIXED_BYTES = 4 * (2 * JET_FLOATS + S_FLOATS) + 1024;
   static constexpr int NSTAGE_FIT = (225 * 1024 - FIXED_BYTES) / STAGE_BYTES;
-  static constexpr int NSTAGE = NSTAGE_FIT > 6 ? 6 : NSTAGE_FIT;
+  static constexpr int NSTAGE = NSTAGE_FIT > 8 ? 8 : NSTAGE_FIT;
   static constexpr int SMEM_BYTES = NSTAGE * STAGE_BYTES + FIXED_BYTES;
   static constexpr uint32_t TMEM_COLS = tc_tmem_cols(2 * N);
   static_assert(N % 16 == 0 && N <= 256, "bad N");
-  static_assert(NP % SLICE_P == 0 && (SLICE_P * C) % 8 == 0, "bad slice");
-  static_assert(NSTAGE >= 2, "shared memory budget");
+  static_assert(NP % SLICE_P == 0 && (SLICE_P * C) % 16 == 0, "bad slice");
+  static_assert(NSTAGE >= 3, "shared memory budget");
   static_assert(STAGE_BYTES % 128 == 0, "TMA boxes after the stages need 128-B alignment");
 };
-constexpr int DGR_THREADS = 32 * 10;   // 4 generator warps, 4 epilogue warps, MMA warp, producer warp
-constexpr int DGR_EPI_WARP0 = 4, DGR_MMA_WARP = 8;
+constexpr int DGR_EPI_WARPS = 8;       // two epilogue warps per TMEM lane quadrant
+constexpr int DGR_THREADS = 32 * (DGR_EPI_WARPS + 2);   // + MMA warp + producer warp
+constexpr int DGR_MMA_WARP = DGR_EPI_WARPS, DGR_PROD_WARP = DGR_EPI_WARPS + 1;
 
 // W^T tiles for k_dgrad_tc: for M-tile mt (inputs mt*IPT ...), K-block kb (o = kb*KB ...):
 // [hi | lo] each [2 chunks][128 rows][8] bf16, row = il*B + n (il < IPT), zero outside.
@@ -73,19 +71,19 @@ __global__ void k_tile_w_dgr(const float* __restrict__ W, uint16_t* __restrict__
 
 template <int NF, int NS, int M, int OT>
 __global__ void __launch_bounds__(DGR_THREADS, 1)
-    k_dgrad_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmY,
+    k_dgrad_tc(const __grid_constant__ CUtensorMap tmX, const uint16_t* __restrict__ Ysplit,
                const uint16_t* __restrict__ Wtiled, float* __restrict__ Xbar, int64_t P, int I, int IPT, int nmt,
                BasisCfg bc) {
   using Cfg = DgrCfg<NF, NS, M, OT>;
-  constexpr int C = Cfg::C, NP = Cfg::NP, N = Cfg::N, O = Cfg::O, NKB = Cfg::NKB, NSTAGE = Cfg::NSTAGE;
-  constexpr int SLICE_P = Cfg::SLICE_P, ACSB = Cfg::ACSB;
+  constexpr int C = Cfg::C, NP = Cfg::NP, N = Cfg::N, NKB = Cfg::NKB, NSTAGE = Cfg::NSTAGE;
+  constexpr int SLICE_P = Cfg::SLICE_P;
+  constexpr int NEPI = 32 * DGR_EPI_WARPS;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  float* raw = reinterpret_cast<float*>(smem + NSTAGE * Cfg::STAGE_BYTES);   // [2][NP][C][KB]   Ybar boxes
-  float* jets = raw + 2 * Cfg::RAW_FLOATS;                    // [2][NP][C][IPTB] input-jet boxes
+  float* jets = reinterpret_cast<float*>(smem + NSTAGE * Cfg::STAGE_BYTES);   // [2][NP][C][IPTB] input jets
   float* S = jets + 2 * Cfg::JET_FLOATS;                      // epilogue slice [SLICE_P*C][DGR_SST]
   __shared__ __align__(8) uint64_t full_bar[NSTAGE], empty_bar[NSTAGE], acc_full[2], acc_empty[2];
-  __shared__ __align__(8) uint64_t raw_full[2], raw_empty[2], jet_full[2], jet_empty[2];
+  __shared__ __align__(8) uint64_t jet_full[2], jet_empty[2];
   __shared__ uint32_t tmem_base_sh;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t p0 = (int64_t)blockIdx.x * NP;
@@ -93,16 +91,14 @@ __global__ void __launch_bounds__(DGR_THREADS, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < NSTAGE; ++s) {
-      tc::mbar_init(&full_bar[s], TC_GEN_THREADS + 1);
+      tc::mbar_init(&full_bar[s], 1);
       tc::mbar_init(&empty_bar[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       tc::mbar_init(&acc_full[a], 1);
-      tc::mbar_init(&acc_empty[a], 128);
-      tc::mbar_init(&raw_full[a], 1);
-      tc::mbar_init(&raw_empty[a], 4);     // one elected lane per generator warp
+      tc::mbar_init(&acc_empty[a], NEPI);
       tc::mbar_init(&jet_full[a], 1);
-      tc::mbar_init(&jet_empty[a], 4);     // one elected lane per epilogue warp
+      tc::mbar_init(&jet_empty[a], DGR_EPI_WARPS);   // one elected lane per epilogue warp
     }
     tc::fence_mbar_init();
   }
@@ -112,53 +108,11 @@ __global__ void __launch_bounds__(DGR_THREADS, 1)
   tc::tc_fence_after();
   const uint32_t tmem = tmem_base_sh;
 
-  if (warp < 4) {
-    // ===================== generators: TMA'd Ybar box -> bf16 hi/lo -> operand [2 chunks][N rows][8]
-    // task = (row, chunk h), chunk fastest: two float4 reads of the box, one 16-B store per half,
-    // conflict-free on the padded operand.
-    constexpr int NTASK = N * 2;
-    constexpr int TPT = (NTASK + TC_GEN_THREADS - 1) / TC_GEN_THREADS;
-    const int tid = threadIdx.x;
-    const int h = tid & 1;
-    for (int g = 0; g < nblk; ++g) {
-      const int rs = g & 1;
-      tc::mbar_wait(&raw_full[rs], (uint32_t)((g >> 1) & 1));
-      float v[TPT][8];
-#pragma unroll
-      for (int u = 0; u < TPT; ++u) {
-        const int task = tid + u * TC_GEN_THREADS;
-        float4 p = make_float4(0.f, 0.f, 0.f, 0.f), q = p;
-        if (task < NTASK) {
-          const float* src = raw + rs * Cfg::RAW_FLOATS + (task >> 1) * TC_KB + 8 * h;
-          p = *reinterpret_cast<const float4*>(src);
-          q = *reinterpret_cast<const float4*>(src + 4);
-        }
-        v[u][0] = p.x; v[u][1] = p.y; v[u][2] = p.z; v[u][3] = p.w;
-        v[u][4] = q.x; v[u][5] = q.y; v[u][6] = q.z; v[u][7] = q.w;
-      }
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(&raw_empty[rs]);
-      const int s = g % NSTAGE;
-      tc::mbar_wait(&empty_bar[s], ((g / NSTAGE) & 1) ^ 1);
-      uint8_t* y_hi = smem + s * Cfg::STAGE_BYTES + Cfg::W_STAGE_BYTES;
-      uint8_t* y_lo = y_hi + 2 * ACSB;
-#pragma unroll
-      for (int u = 0; u < TPT; ++u) {
-        const int task = tid + u * TC_GEN_THREADS;
-        if (task >= NTASK) break;
-        const int row = task >> 1;
-        uint4 hh, ll;
-        tc::split8_bf16(v[u], hh, ll);
-        *reinterpret_cast<uint4*>(y_hi + h * ACSB + row * 16) = hh;
-        *reinterpret_cast<uint4*>(y_lo + h * ACSB + row * 16) = ll;
-      }
-      tc::fence_proxy_async_smem();
-      tc::mbar_arrive(&full_bar[s]);
-    }
-  } else if (warp < DGR_MMA_WARP) {
+  if (warp < DGR_EPI_WARPS) {
     // ===================== epilogue: per M-tile, TMEM -> smem slices -> jet-chain gather
-    const int qw = warp - DGR_EPI_WARP0;          // TMEM lane quadrant (warp % 4)
-    const int etid = threadIdx.x - 32 * DGR_EPI_WARP0;
+    const int qw = warp & 3;                      // TMEM lane quadrant (warp % 4)
+    const int half = warp >> 2;                   // which half of the slice columns this warp drains
+    const int etid = threadIdx.x;
     const int r = qw * 32 + lane;                 // accumulator row = il*B + n
     for (int mt = 0; mt < nmt; ++mt) {
       const int buf = mt & 1;
@@ -171,7 +125,7 @@ __global__ void __launch_bounds__(DGR_THREADS, 1)
       for (int sl = 0; sl < NP / SLICE_P; ++sl) {
         const uint32_t tb = tmem + ((uint32_t)(qw * 32) << 16) + (uint32_t)(buf * N + sl * SLICE_P * C);
 #pragma unroll 1
-        for (int c8 = 0; c8 < SLICE_P * C; c8 += 8) {
+        for (int c8 = half * 8; c8 < SLICE_P * C; c8 += 16) {
           float v[8];
           tc::tmem_ld8(tb + c8, v);
 #pragma unroll
@@ -181,9 +135,9 @@ __global__ void __launch_bounds__(DGR_THREADS, 1)
           tc::tc_fence_before();
           tc::mbar_arrive(&acc_empty[buf]);
         }
-        tc::named_bar_sync(1, 128);
+        tc::named_bar_sync(1, NEPI);
         // task = (point pq, input il), input fastest: Xbar stores run along i
-        for (int task = etid; task < SLICE_P * n_in; task += 128) {
+        for (int task = etid; task < SLICE_P * n_in; task += NEPI) {
           const int il = task % n_in, pq = task / n_in;
           const int pl = sl * SLICE_P + pq;
           const int64_t p = p0 + pl;
@@ -234,7 +188,7 @@ __global__ void __launch_bounds__(DGR_THREADS, 1)
 #pragma unroll
           for (int a = 0; a < NS; ++a) out[(1 + NF + a) * I] = ddxb[a];
         }
-        tc::named_bar_sync(1, 128);
+        tc::named_bar_sync(1, NEPI);
       }
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&jet_empty[buf]);
@@ -255,11 +209,11 @@ __global__ void __launch_bounds__(DGR_THREADS, 1)
           const uint32_t w_hi = tc::smem_u32(smem + s * Cfg::STAGE_BYTES);
           const uint32_t w_lo = w_hi + 2 * 128 * 16;
           const uint32_t y_hi = w_hi + Cfg::W_STAGE_BYTES;
-          const uint32_t y_lo = y_hi + 2 * ACSB;
+          const uint32_t y_lo = y_hi + 2 * N * 16;
           const uint64_t wh = tc::smem_desc(w_hi, 128 * 16, 128);
           const uint64_t wl = tc::smem_desc(w_lo, 128 * 16, 128);
-          const uint64_t yh = tc::smem_desc(y_hi, ACSB, 128);
-          const uint64_t yl = tc::smem_desc(y_lo, ACSB, 128);
+          const uint64_t yh = tc::smem_desc(y_hi, N * 16, 128);
+          const uint64_t yl = tc::smem_desc(y_lo, N * 16, 128);
           const uint32_t d = tmem + (uint32_t)(buf * N);
           tc::mma_bf16(d, wl, yh, idesc, kb > 0 ? 1u : 0u);
           tc::mma_bf16(d, wh, yl, idesc, 1u);
@@ -271,16 +225,12 @@ __global__ void __launch_bounds__(DGR_THREADS, 1)
     }
     __syncwarp();
   } else {
-    // ===================== producer: Ybar boxes (TMA), W^T stages (bulk copy), input-jet boxes (TMA)
+    // ===================== producer: W^T and pre-split Ybar stages (1-D bulk copies), jet boxes (TMA)
     if (lane == 0) {
       tc::tma_prefetch_desc(&tmX);
-      tc::tma_prefetch_desc(&tmY);
+      const uint16_t* ytile = Ysplit + (int64_t)blockIdx.x * NKB * (Cfg::Y_STAGE_BYTES / 2);
       for (int g = 0; g < nblk; ++g) {
         const int mt = g / NKB, kb = g - (g / NKB) * NKB;
-        const int rs = g & 1;
-        if (g >= 2) tc::mbar_wait(&raw_empty[rs], (uint32_t)(((g >> 1) - 1) & 1));
-        tc::mbar_arrive_expect_tx(&raw_full[rs], Cfg::RAW_FLOATS * 4);
-        tc::tma_load_3d(raw + rs * Cfg::RAW_FLOATS, &tmY, kb * TC_KB, 0, (int)p0, &raw_full[rs]);
         if (kb == 0) {
           const int jb = mt & 1;
           if (mt >= 2) tc::mbar_wait(&jet_empty[jb], (uint32_t)(((mt >> 1) - 1) & 1));
@@ -289,9 +239,11 @@ __global__ void __launch_bounds__(DGR_THREADS, 1)
         }
         const int s = g % NSTAGE;
         tc::mbar_wait(&empty_bar[s], ((g / NSTAGE) & 1) ^ 1);
-        tc::mbar_arrive_expect_tx(&full_bar[s], Cfg::W_STAGE_BYTES);
+        tc::mbar_arrive_expect_tx(&full_bar[s], Cfg::STAGE_BYTES);
         tc::bulk_g2s(smem + s * Cfg::STAGE_BYTES, Wtiled + (int64_t)g * (Cfg::W_STAGE_BYTES / 2), Cfg::W_STAGE_BYTES,
                      &full_bar[s]);
+        tc::bulk_g2s(smem + s * Cfg::STAGE_BYTES + Cfg::W_STAGE_BYTES, ytile + (int64_t)kb * (Cfg::Y_STAGE_BYTES / 2),
+                     Cfg::Y_STAGE_BYTES, &full_bar[s]);
       }
     }
     __syncwarp();

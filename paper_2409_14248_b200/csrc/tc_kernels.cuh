@@ -31,8 +31,8 @@ constexpr int TC_GEN_THREADS = 128;   // one generator group (4 warps); the grou
 constexpr int TC_NGEN = 2;            // generator groups (both also drain the accumulators)
 constexpr int TC_MMA_WARP = 4 * TC_NGEN, TC_PROD_WARP = 4 * TC_NGEN + 1, TC_WIN_WARP = 4 * TC_NGEN + 2;
 constexpr int TC_THREADS = 32 * (4 * TC_NGEN + 3);   // + MMA warp + W producer warp + jet-window TMA warp
-constexpr int TC_WIN = 8;             // inputs per jet window
-constexpr int TC_NWIN = 4;            // jet-window ring depth
+constexpr int TC_WIN = 4;             // inputs per jet window (16-B TMA rows)
+constexpr int TC_NWIN = 8;            // jet-window ring depth
 
 // Points per tile so that N = NP*C is a multiple of 16 and <= 256.
 __host__ __device__ constexpr int tc_np(int C) {
@@ -56,7 +56,8 @@ struct FwdCfg {
   static constexpr int W_STAGE_BYTES = 2 * 2 * O * 16;       // hi + lo, [2 chunks][O rows][8] each
   static constexpr int A_STAGE_BYTES = 2 * 2 * ACSB;         // hi + lo, [2 chunks][N rows][8] each
   static constexpr int STAGE_BYTES = W_STAGE_BYTES + A_STAGE_BYTES;
-  static constexpr int WIN_FLOATS = NP * C * TC_WIN;         // TMA box [NP points][C][TC_WIN inputs]
+  static constexpr int CB = C | 1;                           // box channels (odd: conflict-free window reads)
+  static constexpr int WIN_FLOATS = NP * CB * TC_WIN;        // TMA box [NP points][CB][TC_WIN inputs]
   static constexpr int FIXED_BYTES = 4 * TC_NWIN * WIN_FLOATS + 4 * 256 + 1024;
   static constexpr int NSTAGE_FIT = (225 * 1024 - FIXED_BYTES) / STAGE_BYTES;   // static smem + margin
   static constexpr int NSTAGE = NSTAGE_FIT > 6 ? 6 : NSTAGE_FIT;
@@ -205,12 +206,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       while (next_drain < nseg - 1 && kb >= (next_drain + 1) * seg + NSTAGE) drain(next_drain++);
       // windows: release those below this K-block's first input, wait for those up to its last
       const int ihi = min(I - 1, ilo + (nlo + TC_KB - 1 >= B) + (nlo + TC_KB - 1 >= 2 * B));
-      while (wrel < (ilo >> 3)) {
+      while (wrel < ilo / TC_WIN) {
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&win_empty[wrel % TC_NWIN]);
         ++wrel;
       }
-      while (wwait <= (ihi >> 3)) {
+      while (wwait <= ihi / TC_WIN) {
         tc::mbar_wait(&win_full[wwait % TC_NWIN], (uint32_t)((wwait / TC_NWIN) & 1));
         ++wwait;
       }
@@ -229,7 +230,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int i = i0 + h;
-          const float* wp = win + ((i / TC_WIN) % TC_NWIN) * Cfg::WIN_FLOATS + (pl * C) * TC_WIN + (i % TC_WIN);
+          const float* wp = win + ((i / TC_WIN) % TC_NWIN) * Cfg::WIN_FLOATS + (pl * Cfg::CB) * TC_WIN + (i % TC_WIN);
           jx[h] = wp[0];
 #pragma unroll
           for (int a = 0; a < NF; ++a) jdx[h][a] = wp[(1 + a) * TC_WIN];
@@ -346,6 +347,57 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 
 namespace {
 
+// Pre-split the output-jet adjoint Ybar[P][C][O] of a tensor-core layer into the bf16 hi/lo operand
+// stages both reverse kernels bulk-copy (every CTA of k_wgrad_tc and every
+// M-tile of k_dgrad_tc would otherwise re-split the same values):
+//   YW (k_wgrad_tc B operand, K = 8 points x channel pair):
+//       [8-point block b][stage ss][hi|lo][chunk ch = channel 2ss+ch][O rows][8 points]
+//   YD (k_dgrad_tc B operand, K = 16 outputs):
+//       [point tile t (NP points)][K-block kb][hi|lo][chunk = 8 outputs][N rows = p*C + c][8]
+// One block per 8 points; the block stages Ybar[8][C][O] in shared memory (coalesced float4 loads).
+template <int C, int O>
+__global__ void __launch_bounds__(256) k_split_ybar(const float* __restrict__ Ybar, int64_t P,
+                                                    uint16_t* __restrict__ YW, uint16_t* __restrict__ YD) {
+  constexpr int NSB = (C + 1) / 2, NP = tc_np(C), N = NP * C, NKB = O / TC_KB;
+  extern __shared__ float ys[];   // [8][C][O]
+  const int64_t b = blockIdx.x;
+  const int64_t p0 = b * 8;
+  const float4* src = reinterpret_cast<const float4*>(Ybar + p0 * (int64_t)(C * O));
+  for (int e = threadIdx.x; e < 8 * C * O / 4; e += blockDim.x) {
+    const int q = (e * 4) / (C * O);
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (p0 + q < P) v = __ldg(src + e);
+    reinterpret_cast<float4*>(ys)[e] = v;
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < NSB * 2 * O; t += blockDim.x) {
+    const int o = t % O, ch = (t / O) & 1, ss = t / (2 * O);
+    const int c = 2 * ss + ch;
+    float v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v[q] = (c < C) ? ys[(q * C + c) * O + o] : 0.f;
+    uint4 hi, lo;
+    tc::split8_bf16(v, hi, lo);
+    uint16_t* dst = YW + (b * NSB + ss) * (int64_t)(2 * 2 * O * 8);
+    *reinterpret_cast<uint4*>(dst + (ch * O + o) * 8) = hi;
+    *reinterpret_cast<uint4*>(dst + 2 * O * 8 + (ch * O + o) * 8) = lo;
+  }
+  for (int t = threadIdx.x; t < 8 * C * (O / 8); t += blockDim.x) {
+    const int og = t % (O / 8), c = (t / (O / 8)) % C, q = t / ((O / 8) * C);
+    const int64_t p = p0 + q;
+    const int64_t tile = p / NP;
+    const int row = (int)(p - tile * NP) * C + c;
+    float v[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) v[e] = ys[(q * C + c) * O + og * 8 + e];
+    uint4 hi, lo;
+    tc::split8_bf16(v, hi, lo);
+    uint16_t* dst = YD + (tile * NKB + og / 2) * (int64_t)(2 * 2 * N * 8);
+    *reinterpret_cast<uint4*>(dst + ((og & 1) * N + row) * 8) = hi;
+    *reinterpret_cast<uint4*>(dst + 2 * N * 8 + ((og & 1) * N + row) * 8) = lo;
+  }
+}
+
 // ---------------------------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------------------------
@@ -357,7 +409,7 @@ bool tc_layer_ok(const hrkan_net* net, int l) {
   if (O != 128 && O != 256) return false;
   if (net->engine == 0 && (int64_t)I * net->B < 256) return false;   // K too small to pay off
   if (net->B < 8) return false;                   // a K chunk spans at most 2 inputs; <= 17 inputs per M-tile
-  if (I % 8 != 0) return false;                    // jet windows of 8 inputs (TMA rows 16-B aligned)
+  if (I % 8 != 0) return false;                    // jet windows / boxes (TMA rows 16-B aligned)
   return true;
 }
 
@@ -402,7 +454,7 @@ hrkan_status launch_fwd_tc(hrkan_net* net, int l, const float* X, float* Y, int6
   }
   const int I = net->widths[l];
   CUtensorMap tm;
-  HR_TRY(make_tmap_f32_3d(&tm, X, (uint64_t)I, (uint64_t)Cfg::C, (uint64_t)n, TC_WIN, Cfg::C, Cfg::NP));
+  HR_TRY(make_tmap_f32_3d(&tm, X, (uint64_t)I, (uint64_t)Cfg::C, (uint64_t)n, TC_WIN, Cfg::CB, Cfg::NP));
   const TcLayerState& ls = net->tc_layers[l];
   const unsigned grid = (unsigned)((n + Cfg::NP - 1) / Cfg::NP);
   const int cls = HRKAN_K_FWD_HIDDEN;
@@ -425,6 +477,35 @@ hrkan_status tc_forward_layer(hrkan_net* net, int l, const float* X, float* Y, i
     else HR_TRY(launch_fwd_tc<NF, NS, M, 2>(net, l, X, Y, n, st));
     *done = true;
     return HRKAN_OK;
+  }
+}
+
+// Pre-split Ybar of tensor-core layer l for both reverse kernels (net->tc_yw, net->tc_yd).
+template <int NF, int NS, int M>
+hrkan_status tc_split_ybar(hrkan_net* net, int l, const float* Ybar, int64_t n, cudaStream_t st) {
+  constexpr int C = 1 + NF + NS;
+  if constexpr (tc_np(C) == 0) {
+    return HRKAN_OK;
+  } else {
+    if (!tc_layer_ok(net, l) || n <= 0) return HRKAN_OK;
+    const int O = net->widths[l + 1];
+    const int64_t nb8 = (n + 7) / 8;
+    const int64_t ntile = (n + tc_np(C) - 1) / tc_np(C);
+    const size_t yw = (size_t)nb8 * ((C + 1) / 2) * 2 * 2 * O * 8;
+    const size_t yd = (size_t)ntile * (O / TC_KB) * 2 * 2 * tc_np(C) * C * 8;
+    HR_CUDA(net->tc_yw.ensure(yw * sizeof(uint16_t)));
+    HR_CUDA(net->tc_yd.ensure(yd * sizeof(uint16_t)));
+    auto launch = [&](auto OC) -> hrkan_status {
+      constexpr int OO = decltype(OC)::value;
+      auto kfn = k_split_ybar<C, OO>;
+      constexpr int smem = 8 * C * OO * 4;
+      if (smem > 48 * 1024) HR_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      HR_LAUNCH(HRKAN_K_OTHER, "k_split_ybar",
+                kfn<<<(unsigned)nb8, 256, smem, st>>>(Ybar, n, (uint16_t*)net->tc_yw.p, (uint16_t*)net->tc_yd.p));
+      return HRKAN_OK;
+    };
+    if (O == 128) return launch(std::integral_constant<int, 128>{});
+    return launch(std::integral_constant<int, 256>{});
   }
 }
 
@@ -451,12 +532,11 @@ hrkan_status launch_wgrad_tc(hrkan_net* net, int l, const float* X, const float*
   HR_CUDA(net->tc_ws.ensure(part_bytes));
   float* part = net->tc_ws.f();
   float* part_b = part + (size_t)nslab * O * K;
-  CUtensorMap tmX, tmY;
+  CUtensorMap tmX;
   HR_TRY(make_tmap_f32_3d(&tmX, X, (uint64_t)I, (uint64_t)C, (uint64_t)n, WGR_IW, C, WGR_JP));
-  HR_TRY(make_tmap_f32_3d(&tmY, Ybar, (uint64_t)O, (uint64_t)C, (uint64_t)n, O, 2, 8));
   HR_LAUNCH(HRKAN_K_WGRAD_HIDDEN, "k_wgrad_tc",
-            kfn<<<(unsigned)(nslab * nmt), WGR_THREADS, Cfg::SMEM_BYTES, st>>>(tmX, tmY, part, n, I, nmt, slab,
-                                                                               net->tc_wseg, net->bc));
+            kfn<<<(unsigned)(nslab * nmt), WGR_THREADS, Cfg::SMEM_BYTES, st>>>(
+                tmX, (const uint16_t*)net->tc_yw.p, part, n, I, nmt, slab, net->tc_wseg, net->bc));
   HR_LAUNCH(HRKAN_K_REDUCE, "k_reduce_slabs",
             k_reduce_slabs<<<(unsigned)((O * K + 255) / 256), 256, 0, st>>>(part, nslab, (int64_t)O * K, dW));
   const int nz = (int)std::min<int64_t>(1024, std::max<int64_t>(1, n / 256));
@@ -490,13 +570,12 @@ hrkan_status launch_dgrad_tc(hrkan_net* net, int l, const float* X, const float*
   }
   const TcLayerState& ls = net->tc_layers[l];
   const int I = net->widths[l];
-  CUtensorMap tmX, tmY;
+  CUtensorMap tmX;
   HR_TRY(make_tmap_f32_3d(&tmX, X, (uint64_t)I, (uint64_t)Cfg::C, (uint64_t)n, DGR_IPTB, Cfg::C, Cfg::NP));
-  HR_TRY(make_tmap_f32_3d(&tmY, Ybar, (uint64_t)Cfg::O, (uint64_t)Cfg::C, (uint64_t)n, TC_KB, Cfg::C, Cfg::NP));
   const unsigned grid = (unsigned)((n + Cfg::NP - 1) / Cfg::NP);
   HR_LAUNCH(HRKAN_K_DGRAD_HIDDEN, "k_dgrad_tc",
-            kfn<<<grid, DGR_THREADS, Cfg::SMEM_BYTES, st>>>(tmX, tmY, ls.w_dgr, Xbar, n, I, 128 / net->B, ls.ntile_dgr,
-                                                            net->bc));
+            kfn<<<grid, DGR_THREADS, Cfg::SMEM_BYTES, st>>>(tmX, (const uint16_t*)net->tc_yd.p, ls.w_dgr, Xbar, n, I,
+                                                            128 / net->B, ls.ntile_dgr, net->bc));
   return HRKAN_OK;
 }
 
