@@ -28,7 +28,7 @@ using namespace hrkan;
 
 constexpr int TC_KB = 16;          // K per pipeline stage (two tf32 MMA K-steps of 8)
 constexpr int TC_GEN_THREADS = 128;   // one generator group (4 warps); the group handles every other K-block
-constexpr int TC_NGEN = 2;            // generator groups (both also drain the accumulators)
+constexpr int TC_NGEN = 3;            // generator groups (all also drain the accumulators)
 constexpr int TC_MMA_WARP = 4 * TC_NGEN, TC_PROD_WARP = 4 * TC_NGEN + 1, TC_WIN_WARP = 4 * TC_NGEN + 2;
 constexpr int TC_THREADS = 32 * (4 * TC_NGEN + 3);   // + MMA warp + W producer warp + jet-window TMA warp
 constexpr int TC_WIN = 4;             // inputs per jet window (16-B TMA rows)
@@ -523,7 +523,17 @@ hrkan_status launch_wgrad_tc(hrkan_net* net, int l, const float* X, const float*
   const int I = net->widths[l];
   const int64_t K = (int64_t)I * net->B;
   const int nmt = (int)((K + 127) / 128);
-  int nslab = (int)std::max<int64_t>(1, (4 * net->num_sms + nmt / 2) / nmt);
+  // slabs per M-tile: 3-6 waves of one CTA per SM, chosen to minimise the idle tail of the last wave
+  int nslab = 1;
+  {
+    double best = -1.0;
+    const int lo = std::max(1, (3 * net->num_sms) / nmt), hi = std::max(lo, (6 * net->num_sms) / nmt);
+    for (int c = lo; c <= hi; ++c) {
+      const int64_t units = (int64_t)c * nmt;
+      const double eff = (double)units / (double)(((units + net->num_sms - 1) / net->num_sms) * net->num_sms);
+      if (eff > best + 1e-9) { best = eff; nslab = c; }
+    }
+  }
   nslab = (int)std::min<int64_t>(nslab, std::max<int64_t>(1, n / 64));
   int64_t slab = (n + nslab - 1) / nslab;
   slab = (slab + WGR_JP - 1) / WGR_JP * WGR_JP;       // jet boxes of 32 points never straddle slabs
