@@ -125,6 +125,7 @@ struct hrkan_net {
   std::vector<TcLayerState> tc_layers;
   int tc_seg = 32;                      // K-blocks per TMEM accumulation segment (precision bound)
   int tc_wseg = 256;                    // wgrad stages per TMEM drain into the fp32 master
+  int tc_dbg = 0;                       // timing-experiment switches (HRKAN_TC_DBG; 0 in production)
   // device-time profiling (hrkan_profile_enable / hrkan_profile_read)
   struct ProfEv { cudaEvent_t a, b; int cls; };
   bool prof_on = false;

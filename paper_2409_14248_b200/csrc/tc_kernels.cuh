@@ -96,7 +96,7 @@ __global__ void k_tile_w_fwd(const float* __restrict__ W, uint16_t* __restrict__
 template <int NF, int NS, int M, int NMT>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     k_fwd_tc(const __grid_constant__ CUtensorMap tmX, const uint16_t* __restrict__ Wtiled, const float* __restrict__ bias,
-             float* __restrict__ Y, int64_t P, int I, int nkb, int seg, BasisCfg bc) {
+             float* __restrict__ Y, int64_t P, int I, int nkb, int seg, BasisCfg bc, int dbg) {
   using Cfg = FwdCfg<NF, NS, M, NMT>;
   constexpr int C = Cfg::C, NP = Cfg::NP, N = Cfg::N, O = Cfg::O, NACC = Cfg::NACC, NSTAGE = Cfg::NSTAGE;
   constexpr int ACSB = Cfg::ACSB;
@@ -223,7 +223,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 #pragma unroll
       for (int u = 0; u < TPT; ++u) {
         const int task = gtid + u * TC_GEN_THREADS;
-        if (task >= NTASK) break;
+        if (task >= NTASK || (dbg & 1)) break;    // dbg bit 0: skip generation (timing experiments only)
         const int pl = task >> 2;
         // jets of inputs i0 and i0+1 (the chunk crosses into i0+1 when n0 + 3 >= B)
         float jx[2], jdx[2][NF > 0 ? NF : 1], jddx[2][NS > 0 ? NS : 1];
@@ -460,7 +460,8 @@ hrkan_status launch_fwd_tc(hrkan_net* net, int l, const float* X, float* Y, int6
   const int cls = HRKAN_K_FWD_HIDDEN;
   HR_LAUNCH(cls, "k_fwd_tc",
             kfn<<<grid, TC_THREADS, Cfg::SMEM_BYTES, st>>>(tm, ls.w_fwd, net->params + net->b_off[l], Y, n, I, ls.nkb,
-                                                           Cfg::NACC == 2 ? net->tc_seg : 2 * net->tc_seg, net->bc));
+                                                           Cfg::NACC == 2 ? net->tc_seg : 2 * net->tc_seg, net->bc,
+                                                           net->tc_dbg));
   return HRKAN_OK;
 }
 
