@@ -75,7 +75,7 @@ def class_flops(w: HI.Workload, n_int: int, n_bi: int, c_int: int):
 def tensor_core_layers(w: HI.Workload, engine: int) -> bool:
     """True when the hidden layers run on the tcgen05 kernels (libhrkan's tc_layer_ok rule)."""
     hidden = [(w.widths[l], w.widths[l + 1]) for l in range(1, len(w.widths) - 2)]
-    return engine != 1 and bool(hidden) and all(O in (128, 256) and I % 8 == 0 and
+    return engine != 1 and bool(hidden) and all(O in (64, 128, 256) and I % 8 == 0 and
                                                 (engine == 2 or I * w.B >= 256) and w.B >= 8 for I, O in hidden)
 
 

@@ -20,12 +20,12 @@ __host__ __device__ constexpr int dgr_slice_p(int C) { return C == 1 ? 64 : 16; 
 constexpr int DGR_SST = 129;   // column stride of the epilogue slice (odd: conflict-free gathers)
 constexpr int DGR_IPTB = 16;   // jet box width (inputs) >= IPT + 3 (box start aligned down to 16 B), B >= 11
 
-template <int NF, int NS, int M, int OT>
+template <int NF, int NS, int M, int OO>
 struct DgrCfg {
   static constexpr int C = 1 + NF + NS;
   static constexpr int NP = tc_np(C);
   static constexpr int N = NP * C;
-  static constexpr int O = 128 * OT;
+  static constexpr int O = OO;                                // = MMA K of this kernel (64, 128, 256)
   static constexpr int NKB = O / TC_KB;
   static constexpr int W_STAGE_BYTES = 2 * 2 * 128 * 16;      // W^T hi + lo, [2 chunks][128 rows][8] bf16
   static constexpr int Y_STAGE_BYTES = 2 * 2 * N * 16;        // Ybar hi + lo, [2 chunks][N rows][8] bf16
@@ -69,12 +69,12 @@ __global__ void k_tile_w_dgr(const float* __restrict__ W, uint16_t* __restrict__
   dst[per + r8] = lo;
 }
 
-template <int NF, int NS, int M, int OT>
+template <int NF, int NS, int M, int OO>
 __global__ void __launch_bounds__(DGR_THREADS, 1)
     k_dgrad_tc(const __grid_constant__ CUtensorMap tmX, const uint16_t* __restrict__ Ysplit,
                const uint16_t* __restrict__ Wtiled, float* __restrict__ Xbar, int64_t P, int I, int IPT, int nmt,
                BasisCfg bc) {
-  using Cfg = DgrCfg<NF, NS, M, OT>;
+  using Cfg = DgrCfg<NF, NS, M, OO>;
   constexpr int C = Cfg::C, NP = Cfg::NP, N = Cfg::N, NKB = Cfg::NKB, NSTAGE = Cfg::NSTAGE;
   constexpr int SLICE_P = Cfg::SLICE_P;
   constexpr int NEPI = 32 * DGR_EPI_WARPS;

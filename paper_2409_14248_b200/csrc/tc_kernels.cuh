@@ -43,17 +43,19 @@ __host__ __device__ constexpr uint32_t tc_tmem_cols(uint32_t c) {
   return c <= 32 ? 32 : c <= 64 ? 64 : c <= 128 ? 128 : c <= 256 ? 256 : 512;
 }
 
-template <int NF, int NS, int M, int NMT>
+template <int NF, int NS, int M, int OO>
 struct FwdCfg {
   static constexpr int C = 1 + NF + NS;
   static constexpr int NP = tc_np(C);
   static constexpr int N = NP * C;
-  static constexpr int O = 128 * NMT;
+  static constexpr int O = OO;                               // output neurons (64, 128 or 256)
+  static constexpr int NMT = (OO + 127) / 128;               // 128-row M-tiles
+  static constexpr int OP = 128 * NMT;                       // rows of the W tiles (zero-padded)
   // bf16 operands, K-major, SWIZZLE_NONE: a K-block of 16 = 2 chunks of 8 elements (16 B per row).
   // Generated operand chunk stride padded to 64 B (mod 128 B): the generators' 8-B stores
   // (4 consecutive K of one row, chunk-fastest lanes) are bank-conflict free.
   static constexpr int ACSB = N * 16 + 64;                   // chunk stride (bytes)
-  static constexpr int W_STAGE_BYTES = 2 * 2 * O * 16;       // hi + lo, [2 chunks][O rows][8] each
+  static constexpr int W_STAGE_BYTES = 2 * 2 * OP * 16;      // hi + lo, [2 chunks][OP rows][8] each
   static constexpr int A_STAGE_BYTES = 2 * 2 * ACSB;         // hi + lo, [2 chunks][N rows][8] each
   static constexpr int STAGE_BYTES = W_STAGE_BYTES + A_STAGE_BYTES;
   static constexpr int CB = C | 1;                           // box channels (odd: conflict-free window reads)
@@ -70,16 +72,17 @@ struct FwdCfg {
   static_assert(STAGE_BYTES % 128 == 0, "TMA windows after the stages need 128-B alignment");
 };
 
-// Pre-tiled, pre-split weights for k_fwd_tc: for K-block kb: [hi | lo] each [2 chunks][O][8] bf16.
-__global__ void k_tile_w_fwd(const float* __restrict__ W, uint16_t* __restrict__ Wt, int O, int K, int nkb) {
+// Pre-tiled, pre-split weights for k_fwd_tc: for K-block kb: [hi | lo] each [2 chunks][OP][8] bf16
+// (rows o >= O are zero: a 64-neuron layer runs as one zero-padded 128-row M-tile).
+__global__ void k_tile_w_fwd(const float* __restrict__ W, uint16_t* __restrict__ Wt, int O, int OP, int K, int nkb) {
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int64_t per_kb = (int64_t)O * TC_KB;         // elements of one of hi / lo per K-block
+  const int64_t per_kb = (int64_t)OP * TC_KB;        // elements of one of hi / lo per K-block
   if (t >= per_kb * nkb) return;
   const int kb = (int)(t / per_kb);
-  const int r = (int)(t - (int64_t)kb * per_kb);     // r = (chunk*O + o)*8 + e
-  const int e = r & 7, o = (r >> 3) % O, ch = (r >> 3) / O;
+  const int r = (int)(t - (int64_t)kb * per_kb);     // r = (chunk*OP + o)*8 + e
+  const int e = r & 7, o = (r >> 3) % OP, ch = (r >> 3) / OP;
   const int k = kb * TC_KB + 8 * ch + e;
-  const float w = (k < K) ? W[(int64_t)o * K + k] : 0.f;
+  const float w = (k < K && o < O) ? W[(int64_t)o * K + k] : 0.f;
   uint16_t hi, lo;
   tc::split1_bf16(w, hi, lo);
   uint16_t* dst = Wt + (int64_t)kb * 2 * per_kb;
@@ -93,12 +96,13 @@ __global__ void k_tile_w_fwd(const float* __restrict__ W, uint16_t* __restrict__
 //   warp 9       1-D bulk copies of the pre-tiled W_hi/W_lo stage;
 //   warp 10      TMA loads of jet windows: X[p0 .. p0+NP)[C][8w .. 8w+8) -> smem ring (TC_NWIN deep),
 //                so the generators read the jets from shared memory (coalesced, latency hidden).
-template <int NF, int NS, int M, int NMT>
+template <int NF, int NS, int M, int OO>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     k_fwd_tc(const __grid_constant__ CUtensorMap tmX, const uint16_t* __restrict__ Wtiled, const float* __restrict__ bias,
              float* __restrict__ Y, int64_t P, int I, int nkb, int seg, BasisCfg bc, int dbg) {
-  using Cfg = FwdCfg<NF, NS, M, NMT>;
+  using Cfg = FwdCfg<NF, NS, M, OO>;
   constexpr int C = Cfg::C, NP = Cfg::NP, N = Cfg::N, O = Cfg::O, NACC = Cfg::NACC, NSTAGE = Cfg::NSTAGE;
+  constexpr int NMT = Cfg::NMT, OP = Cfg::OP;
   constexpr int ACSB = Cfg::ACSB;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -149,7 +153,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 #pragma unroll 1
       for (int t = 0; t < NMT; ++t) {
         const int o = t * 128 + qw * 32 + lane;
-        const float b = (sg == 0) ? __ldg(bias + o) : 0.f;
+        const bool o_ok = o < O;
+        const float b = (sg == 0 && o_ok) ? __ldg(bias + o) : 0.f;
         const uint32_t tbase = tmem + ((uint32_t)(qw * 32) << 16) + (uint32_t)((buf * NMT + t) * N);
         // 16-column chunks are shared round-robin by the generator groups (same lane quadrant)
 #pragma unroll 1
@@ -163,7 +168,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             const int col = c0 + q;
             const int c = col / NP, pl = col - c * NP;
             const int64_t p = p0 + pl;
-            ok[q] = p < P;
+            ok[q] = p < P && o_ok;
             yp[q] = Y + (p * C + c) * (int64_t)O + o;
             if (sg == 0 && c == 0) v[q] += b;
           }
@@ -290,7 +295,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         tc::mbar_wait(&full_bar[s], (kb / NSTAGE) & 1);
         tc::tc_fence_after();
         const uint32_t w_hi = tc::smem_u32(smem + s * Cfg::STAGE_BYTES);
-        const uint32_t w_lo = w_hi + 2 * O * 16;
+        const uint32_t w_lo = w_hi + 2 * OP * 16;
         const uint32_t a_hi = w_hi + Cfg::W_STAGE_BYTES;
         const uint32_t a_lo = a_hi + 2 * ACSB;
         // one K-step of 16 per stage: LBO = chunk stride, SBO = 8 rows = 128 B
@@ -298,8 +303,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         const uint64_t bl = tc::smem_desc(a_lo, ACSB, 128);
 #pragma unroll
         for (int t = 0; t < NMT; ++t) {
-          const uint64_t wh = tc::smem_desc(w_hi + t * 128 * 16, O * 16, 128);
-          const uint64_t wl = tc::smem_desc(w_lo + t * 128 * 16, O * 16, 128);
+          const uint64_t wh = tc::smem_desc(w_hi + t * 128 * 16, OP * 16, 128);
+          const uint64_t wl = tc::smem_desc(w_lo + t * 128 * 16, OP * 16, 128);
           const uint32_t d = tmem + (uint32_t)((buf * NMT + t) * N);
           tc::mma_bf16(d, wl, bh, idesc, seg_first ? 0u : 1u);
           tc::mma_bf16(d, wh, bl, idesc, 1u);
@@ -406,7 +411,7 @@ bool tc_layer_ok(const hrkan_net* net, int l) {
   const int L = net->L;
   if (l <= 0 || l >= L - 1) return false;          // hidden layers only
   const int O = net->widths[l + 1], I = net->widths[l];
-  if (O != 128 && O != 256) return false;
+  if (O != 64 && O != 128 && O != 256) return false;
   if (net->engine == 0 && (int64_t)I * net->B < 256) return false;   // K too small to pay off
   if (net->B < 8) return false;                   // a K chunk spans at most 2 inputs; <= 17 inputs per M-tile
   if (I % 8 != 0) return false;                    // jet windows / boxes (TMA rows 16-B aligned)
@@ -421,13 +426,15 @@ hrkan_status tc_refresh_weights(hrkan_net* net, cudaStream_t st) {
     TcLayerState& ls = net->tc_layers[l];
     const int K = I * net->B;
     ls.nkb = (K + TC_KB - 1) / TC_KB;
-    const size_t n = (size_t)ls.nkb * 2 * O * TC_KB;
+    const int OP = (O + 127) / 128 * 128;
+    const size_t n = (size_t)ls.nkb * 2 * OP * TC_KB;
     if (!ls.w_fwd) {
       if (cudaMalloc(&ls.w_fwd, n * sizeof(uint16_t)) != cudaSuccess) return fail(HRKAN_ENOMEM, "tc weight alloc");
     }
-    const int64_t tot = (int64_t)ls.nkb * O * TC_KB;
+    const int64_t tot = (int64_t)ls.nkb * OP * TC_KB;
     HR_LAUNCH(HRKAN_K_OTHER, "k_tile_w_fwd",
-              k_tile_w_fwd<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(net->params + net->w_off[l], ls.w_fwd, O, K, ls.nkb));
+              k_tile_w_fwd<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(net->params + net->w_off[l], ls.w_fwd, O, OP, K,
+                                                                          ls.nkb));
     // W^T tiles for the dgrad kernel (input-aligned M-tiles)
     const int IPT = 128 / net->B;
     ls.ntile_dgr = (I + IPT - 1) / IPT;
@@ -443,10 +450,10 @@ hrkan_status tc_refresh_weights(hrkan_net* net, cudaStream_t st) {
   return HRKAN_OK;
 }
 
-template <int NF, int NS, int M, int NMT>
+template <int NF, int NS, int M, int OO>
 hrkan_status launch_fwd_tc(hrkan_net* net, int l, const float* X, float* Y, int64_t n, cudaStream_t st) {
-  using Cfg = FwdCfg<NF, NS, M, NMT>;
-  auto kfn = k_fwd_tc<NF, NS, M, NMT>;
+  using Cfg = FwdCfg<NF, NS, M, OO>;
+  auto kfn = k_fwd_tc<NF, NS, M, OO>;
   static bool attr_set = false;
   if (!attr_set) {
     HR_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
@@ -474,8 +481,9 @@ hrkan_status tc_forward_layer(hrkan_net* net, int l, const float* X, float* Y, i
   } else {
     if (!tc_layer_ok(net, l) || l >= (int)net->tc_layers.size() || !net->tc_layers[l].w_fwd) return HRKAN_OK;
     const int O = net->widths[l + 1];
-    if (O == 128) HR_TRY(launch_fwd_tc<NF, NS, M, 1>(net, l, X, Y, n, st));
-    else HR_TRY(launch_fwd_tc<NF, NS, M, 2>(net, l, X, Y, n, st));
+    if (O == 64) HR_TRY(launch_fwd_tc<NF, NS, M, 64>(net, l, X, Y, n, st));
+    else if (O == 128) HR_TRY(launch_fwd_tc<NF, NS, M, 128>(net, l, X, Y, n, st));
+    else HR_TRY(launch_fwd_tc<NF, NS, M, 256>(net, l, X, Y, n, st));
     *done = true;
     return HRKAN_OK;
   }
@@ -505,17 +513,18 @@ hrkan_status tc_split_ybar(hrkan_net* net, int l, const float* Ybar, int64_t n, 
                 kfn<<<(unsigned)nb8, 256, smem, st>>>(Ybar, n, (uint16_t*)net->tc_yw.p, (uint16_t*)net->tc_yd.p));
       return HRKAN_OK;
     };
+    if (O == 64) return launch(std::integral_constant<int, 64>{});
     if (O == 128) return launch(std::integral_constant<int, 128>{});
     return launch(std::integral_constant<int, 256>{});
   }
 }
 
-template <int NF, int NS, int M, int OT>
+template <int NF, int NS, int M, int OO>
 hrkan_status launch_wgrad_tc(hrkan_net* net, int l, const float* X, const float* Ybar, float* dW, float* db,
                              int64_t n, cudaStream_t st) {
-  using Cfg = WgrCfg<NF, NS, M, OT>;
+  using Cfg = WgrCfg<NF, NS, M, OO>;
   constexpr int C = Cfg::C, O = Cfg::O;
-  auto kfn = k_wgrad_tc<NF, NS, M, OT>;
+  auto kfn = k_wgrad_tc<NF, NS, M, OO>;
   static bool attr_set = false;
   if (!attr_set) {
     HR_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
@@ -563,17 +572,18 @@ hrkan_status tc_wgrad_layer(hrkan_net* net, int l, const float* X, const float* 
   *done = false;
   if (!tc_layer_ok(net, l) || n < 8) return HRKAN_OK;
   const int O = net->widths[l + 1];
-  if (O == 128) HR_TRY(launch_wgrad_tc<NF, NS, M, 1>(net, l, X, Ybar, dW, db, n, st));
-  else HR_TRY(launch_wgrad_tc<NF, NS, M, 2>(net, l, X, Ybar, dW, db, n, st));
+  if (O == 64) HR_TRY(launch_wgrad_tc<NF, NS, M, 64>(net, l, X, Ybar, dW, db, n, st));
+  else if (O == 128) HR_TRY(launch_wgrad_tc<NF, NS, M, 128>(net, l, X, Ybar, dW, db, n, st));
+  else HR_TRY(launch_wgrad_tc<NF, NS, M, 256>(net, l, X, Ybar, dW, db, n, st));
   *done = true;
   return HRKAN_OK;
 }
 
-template <int NF, int NS, int M, int OT>
+template <int NF, int NS, int M, int OO>
 hrkan_status launch_dgrad_tc(hrkan_net* net, int l, const float* X, const float* Ybar, float* Xbar, int64_t n,
                              cudaStream_t st) {
-  using Cfg = DgrCfg<NF, NS, M, OT>;
-  auto kfn = k_dgrad_tc<NF, NS, M, OT>;
+  using Cfg = DgrCfg<NF, NS, M, OO>;
+  auto kfn = k_dgrad_tc<NF, NS, M, OO>;
   static bool attr_set = false;
   if (!attr_set) {
     HR_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
@@ -601,8 +611,9 @@ hrkan_status tc_dgrad_layer(hrkan_net* net, int l, const float* X, const float* 
     if (!tc_layer_ok(net, l) || l >= (int)net->tc_layers.size() || !net->tc_layers[l].w_dgr) return HRKAN_OK;
     if (128 / net->B + 3 > DGR_IPTB) return HRKAN_OK;   // input-aligned M-tile wider than the jet box
     const int O = net->widths[l + 1];
-    if (O == 128) HR_TRY(launch_dgrad_tc<NF, NS, M, 1>(net, l, X, Ybar, Xbar, n, st));
-    else HR_TRY(launch_dgrad_tc<NF, NS, M, 2>(net, l, X, Ybar, Xbar, n, st));
+    if (O == 64) HR_TRY(launch_dgrad_tc<NF, NS, M, 64>(net, l, X, Ybar, Xbar, n, st));
+    else if (O == 128) HR_TRY(launch_dgrad_tc<NF, NS, M, 128>(net, l, X, Ybar, Xbar, n, st));
+    else HR_TRY(launch_dgrad_tc<NF, NS, M, 256>(net, l, X, Ybar, Xbar, n, st));
     *done = true;
     return HRKAN_OK;
   }
