@@ -218,4 +218,234 @@ __global__ void k_reduce_last(const float* __restrict__ part, int nb, int IB, fl
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Output layer, input-parallel variant (I % 32 == 0, hidden-layer inputs): a block of I/32 warps
+// takes a contiguous range of points in batches of LV_PB; warp w owns inputs [32w, 32w+32) (lane =
+// input, coalesced 128-B rows of the saved jet), so its share of dW lives in the block's shared
+// acc[n][i] columns it alone touches (no atomics; ~I*B*4 bytes per block instead of per warp, which
+// keeps ~48-64 warps per SM in flight to hide the jet-load latency).  Per batch:
+//   pass 1   per point, warp partial jets over its inputs (butterfly) -> smem part[q][w][c];
+//   seeds    thread q < LV_PB sums the warps (fixed order) + bias -> residual, loss, seeds ybar;
+//   pass 2   per point, dW contributions and the input-jet adjoint Xbar (same formulas as above).
+// ---------------------------------------------------------------------------------------------
+constexpr int LV_PB = 4;
+
+template <int NF, int NS, int M, int MODE>
+__global__ void __launch_bounds__(256, 3)
+    k_last_v2(const float* __restrict__ X, const float* __restrict__ W, const float* __restrict__ bias,
+              int64_t P, int I, BasisCfg bc,
+              float* __restrict__ u_out, float* __restrict__ du_out, float* __restrict__ d2u_out,
+              const float* __restrict__ pts, const float* __restrict__ forcing, const float* __restrict__ gtar,
+              float alpha, float adv, float visc, float inv_n,
+              float* __restrict__ Xbar, float* __restrict__ part, int pbm) {
+  constexpr int C = 1 + NF + NS;
+  constexpr int D = (MODE == LAST_POISSON || MODE == LAST_JET) ? NF : 2;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nw = blockDim.x >> 5;                 // = I / 32
+  // pbm <= LV_PB points per batch (host-chosen so that the block's shared memory stays <= 48 KB)
+  const int B = bc.B;
+  const int IB = I * B;
+  extern __shared__ float sm[];
+  float* acc = sm;                                // [B][I]           (not used by LAST_JET)
+  float* wpart = sm + (MODE == LAST_JET ? 0 : IB);   // [LV_PB][nw][C]
+  float* ys = wpart + LV_PB * nw * C;             // [LV_PB][C]
+  float* jsm = ys + LV_PB * C;                    // [nw][pbm][C][32]   this batch's jets
+  __shared__ float red[3][LV_PB];
+  if (MODE != LAST_JET)
+    for (int t = threadIdx.x; t < IB; t += blockDim.x) acc[t] = 0.f;
+  const int64_t lo = (P * blockIdx.x) / gridDim.x, hi = (P * (blockIdx.x + 1)) / gridDim.x;
+  const int i = warp * 32 + lane;
+  float* jw = jsm + warp * (pbm * C * 32) + lane;
+  float db = 0.f, sq = 0.f, bad = 0.f;            // thread q < LV_PB accumulates its batch slot
+  for (int64_t p0 = lo; p0 < hi; p0 += pbm) {
+    const int npb = (int)((hi - p0) < pbm ? (hi - p0) : pbm);
+    __syncthreads();                              // previous batch's seeds and jets consumed
+    // ---------------- stage this batch's jets (all loads in flight together), then pass 1
+    {
+      float v[LV_PB][C];
+#pragma unroll
+      for (int q = 0; q < LV_PB; ++q) {
+        const float* base = X + (p0 + q) * (int64_t)(C * I) + i;
+#pragma unroll
+        for (int c = 0; c < C; ++c) v[q][c] = (q < npb) ? __ldg(base + c * I) : 0.f;
+      }
+#pragma unroll
+      for (int q = 0; q < LV_PB; ++q)
+        if (q < npb) {
+#pragma unroll
+          for (int c = 0; c < C; ++c) jw[(q * C + c) * 32] = v[q][c];
+        }
+    }
+#pragma unroll 1
+    for (int q = 0; q < npb; ++q) {
+      const float* jq = jw + q * C * 32;
+      const float x = jq[0];
+      float s[C];
+#pragma unroll
+      for (int c = 0; c < C; ++c) s[c] = 0.f;
+      if (x != x) s[0] = x;
+      const int n0 = first_basis(x, bc);
+      float T0 = 0.f, T1 = 0.f, T2 = 0.f;
+#pragma unroll
+      for (int r = 0; r < KMAX; ++r) {
+        if (r > bc.k) break;
+        const int n = n0 + r;
+        if (n < 0 || n >= B) continue;
+        float v0, v1, v2, v3;
+        hr_eval<M, (NS > 0 ? 2 : (NF > 0 ? 1 : 0))>(basis_q(x, n, bc), bc.sc, v0, v1, v2, v3);
+        const float w = __ldg(W + i * B + n);
+        T0 = fmaf(w, v0, T0);
+        T1 = fmaf(w, v1, T1);
+        T2 = fmaf(w, v2, T2);
+      }
+      s[0] += T0;
+#pragma unroll
+      for (int a = 0; a < NF; ++a) s[1 + a] = T1 * jq[(1 + a) * 32];
+#pragma unroll
+      for (int a = 0; a < NS; ++a) {
+        const float d1 = jq[(1 + a) * 32], d2 = jq[(1 + NF + a) * 32];
+        s[1 + NF + a] = fmaf(T2 * d1, d1, T1 * d2);
+      }
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s[c] += __shfl_xor_sync(0xffffffffu, s[c], o);
+      }
+      if (lane == 0) {
+#pragma unroll
+        for (int c = 0; c < C; ++c) wpart[(q * nw + warp) * C + c] = s[c];
+      }
+    }
+    __syncthreads();
+    // ---------------- totals, residual, loss, seeds (thread q per point)
+    if (threadIdx.x < npb) {
+      const int q = threadIdx.x;
+      const int64_t p = p0 + q;
+      float s[C];
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        float v = 0.f;
+        for (int w = 0; w < nw; ++w) v += wpart[(q * nw + w) * C + c];
+        s[c] = v;
+      }
+      s[0] += __ldg(bias);
+      if (MODE == LAST_JET) {
+        if (u_out) u_out[p] = s[0];
+#pragma unroll
+        for (int a = 0; a < NF; ++a) {
+          if (du_out) du_out[p * NF + a] = s[1 + a];
+          if (d2u_out) d2u_out[p * NF + a] = s[1 + NF + a];
+        }
+      } else {
+        float y[C];
+#pragma unroll
+        for (int c = 0; c < C; ++c) y[c] = 0.f;
+        float r;
+        if (MODE == LAST_BOUNDARY) {
+          r = s[0] - __ldg(gtar + p);
+          y[0] = 2.f * r * inv_n;
+        } else if (MODE == LAST_BURGERS) {
+          r = s[2] + adv * s[0] * s[1] - visc * s[1 + NF];
+          const float g = 2.f * alpha * r * inv_n;
+          y[0] = g * adv * s[1];
+          y[1] = g * adv * s[0];
+          y[2] = g;
+          y[1 + NF] = -g * visc;
+        } else {
+          float f;
+          if (forcing) {
+            f = __ldg(forcing + p);
+          } else {
+            float prod = 1.f;
+#pragma unroll
+            for (int a = 0; a < D; ++a) prod *= sinpif(__ldg(pts + p * D + a));
+            f = -(float)D * 9.8696044010893586f * prod;   // -D pi^2 prod_a sin(pi xi_a)
+          }
+          float lap = 0.f;
+#pragma unroll
+          for (int a = 0; a < NS; ++a) lap += s[1 + NF + a];
+          r = lap - f;
+          const float g = 2.f * alpha * r * inv_n;
+#pragma unroll
+          for (int a = 0; a < NS; ++a) y[1 + NF + a] = g;
+        }
+        sq = fmaf(r, r, sq);
+        bad += isfinite(r) ? 0.f : 1.f;
+        db += y[0];
+#pragma unroll
+        for (int c = 0; c < C; ++c) ys[q * C + c] = y[c];
+      }
+    }
+    if (MODE == LAST_JET) continue;
+    __syncthreads();
+    // ---------------- pass 2: dW and the adjoint of the input jet (jets from shared memory)
+#pragma unroll 1
+    for (int q = 0; q < npb; ++q) {
+      const int64_t p = p0 + q;
+      const float* jq = jw + q * C * 32;
+      float y[C];
+#pragma unroll
+      for (int c = 0; c < C; ++c) y[c] = ys[q * C + c];
+      const float x = jq[0];
+      float dx[NF > 0 ? NF : 1], ddx[NS > 0 ? NS : 1];
+#pragma unroll
+      for (int a = 0; a < NF; ++a) dx[a] = jq[(1 + a) * 32];
+#pragma unroll
+      for (int a = 0; a < NS; ++a) ddx[a] = jq[(1 + NF + a) * 32];
+      float g1 = 0.f, g2 = 0.f;
+#pragma unroll
+      for (int a = 0; a < NF; ++a) g1 = fmaf(y[1 + a], dx[a], g1);
+#pragma unroll
+      for (int a = 0; a < NS; ++a) {
+        g1 = fmaf(y[1 + NF + a], ddx[a], g1);
+        g2 = fmaf(y[1 + NF + a] * dx[a], dx[a], g2);
+      }
+      const int n0 = first_basis(x, bc);
+      float T1 = 0.f, T2 = 0.f, T3 = 0.f;
+#pragma unroll
+      for (int rr = 0; rr < KMAX; ++rr) {
+        if (rr > bc.k) break;
+        const int n = n0 + rr;
+        if (n < 0 || n >= B) continue;
+        float v0, v1, v2, v3;
+        hr_eval<M, (NS > 0 ? 3 : (NF > 0 ? 2 : 1))>(basis_q(x, n, bc), bc.sc, v0, v1, v2, v3);
+        acc[n * I + i] += fmaf(y[0], v0, fmaf(g1, v1, g2 * v2));
+        const float w = __ldg(W + i * B + n);
+        T1 = fmaf(w, v1, T1);
+        T2 = fmaf(w, v2, T2);
+        T3 = fmaf(w, v3, T3);
+      }
+      float* out = Xbar + p * (int64_t)(C * I) + i;
+      out[0] = fmaf(y[0], T1, fmaf(g1, T2, g2 * T3));
+#pragma unroll
+      for (int a = 0; a < NF; ++a) {
+        float v = y[1 + a] * T1;
+        if (a < NS) v = fmaf(2.f * y[1 + NF + a] * dx[a], T2, v);
+        out[(1 + a) * I] = v;
+      }
+#pragma unroll
+      for (int a = 0; a < NS; ++a) out[(1 + NF + a) * I] = y[1 + NF + a] * T1;
+    }
+  }
+  if (MODE == LAST_JET) return;
+  // ---------------- fixed-order block reduction -> part[block][IB + 4]
+  if (threadIdx.x < LV_PB) {
+    red[0][threadIdx.x] = db;
+    red[1][threadIdx.x] = sq;
+    red[2][threadIdx.x] = bad;
+  }
+  __syncthreads();
+  float* dst = part + (size_t)blockIdx.x * (IB + 4);
+  for (int t = threadIdx.x; t < IB; t += blockDim.x) {
+    const int n = t / I, ii = t - n * I;
+    dst[ii * B + n] = acc[t];                     // flat W layout [i][n]
+  }
+  if (threadIdx.x < 3) {
+    float v = 0.f;
+#pragma unroll
+    for (int q = 0; q < LV_PB; ++q) v += red[threadIdx.x][q];
+    dst[IB + threadIdx.x] = v;
+  }
+}
+
 }  // namespace

@@ -16,6 +16,44 @@ hrkan_status launch_last(hrkan_net* net, const float* in, int64_t n, const PassA
   const int l = net->L - 1;
   const int I = net->widths[l];
   const int IB = I * net->B;
+  constexpr int C = 1 + NF + NS;
+  if (!FIRST && I % 32 == 0 && I <= 256) {
+    // input-parallel variant: I/32 warps per block, block-shared dW accumulator
+    auto kv = k_last_v2<NF, NS, M, MODE>;
+    const int nw = I / 32;
+    const size_t fixed = sizeof(float) * ((MODE == LAST_JET ? 0 : (size_t)IB) + (size_t)LV_PB * nw * C + LV_PB * C);
+    const size_t per_pt = sizeof(float) * (size_t)nw * C * 32;
+    const int pbm = (int)std::max<int64_t>(1, std::min<int64_t>(LV_PB, ((int64_t)47 * 1024 - (int64_t)fixed) / (int64_t)per_pt));
+    const size_t smem = fixed + per_pt * pbm;
+    int per_sm = 0;
+    HR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kv, I, smem));
+    per_sm = std::max(1, per_sm);
+    const int nb = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)per_sm * net->num_sms, (n + LV_PB - 1) / LV_PB));
+    const hrkan_pde* pde = a.pde;
+    if (MODE == LAST_JET) {
+      HR_LAUNCH(HRKAN_K_FWD_LAST, "k_last_v2",
+                kv<<<nb, I, smem, st>>>(in, net->params + net->w_off[l], net->params + net->b_off[l], n, I, net->bc,
+                                        a.u ? a.u + c0 : nullptr, a.du ? a.du + c0 * NF : nullptr,
+                                        a.d2u ? a.d2u + c0 * NF : nullptr, nullptr, nullptr, nullptr, 0.f, 0.f, 0.f, 0.f,
+                                        nullptr, nullptr, pbm));
+      return HRKAN_OK;
+    }
+    HR_CUDA(net->last_part.ensure(sizeof(float) * (size_t)nb * (IB + 4)));
+    const float* pts = a.pts + c0 * net->D;
+    const float* f = a.forcing ? a.forcing + c0 : nullptr;
+    const float* g = a.g ? a.g + c0 : nullptr;
+    const std::string lname = "k_last_v2 (grid " + std::to_string(nb) + ", block " + std::to_string(I) + ", smem " +
+                              std::to_string(smem) + ", per_sm " + std::to_string(per_sm) + ")";
+    HR_LAUNCH(HRKAN_K_FWD_LAST, lname.c_str(),
+              kv<<<nb, I, smem, st>>>(in, net->params + net->w_off[l], net->params + net->b_off[l], n, I, net->bc,
+                                      nullptr, nullptr, nullptr, pts, f, g, pde->alpha, pde->adv, pde->visc, a.inv_n,
+                                      xbar, net->last_part.f(), pbm));
+    const float scale = (MODE == LAST_BOUNDARY) ? a.inv_n : pde->alpha * a.inv_n;
+    HR_LAUNCH(HRKAN_K_REDUCE, "k_reduce_last",
+              k_reduce_last<<<(IB + 3 + 255) / 256, 256, 0, st>>>(net->last_part.f(), nb, IB, a.grad + net->w_off[l],
+                                                                   a.grad + net->b_off[l], scale, a.out_loss, a.out_flag));
+    return HRKAN_OK;
+  }
   auto kfn = k_last_fused<NF, NS, M, MODE, FIRST>;
   if (MODE == LAST_JET) {
     const unsigned grid = (unsigned)std::min<int64_t>(8 * net->num_sms, (n + LF_WARPS - 1) / LF_WARPS);
