@@ -73,7 +73,7 @@ template <int NF, int NS, int M, int OO>
 __global__ void __launch_bounds__(DGR_THREADS, 1)
     k_dgrad_tc(const __grid_constant__ CUtensorMap tmX, const uint16_t* __restrict__ Ysplit,
                const uint16_t* __restrict__ Wtiled, float* __restrict__ Xbar, int64_t P, int I, int IPT, int nmt,
-               BasisCfg bc) {
+               BasisCfg bc, int dbg) {
   using Cfg = DgrCfg<NF, NS, M, OO>;
   constexpr int C = Cfg::C, NP = Cfg::NP, N = Cfg::N, NKB = Cfg::NKB, NSTAGE = Cfg::NSTAGE;
   constexpr int SLICE_P = Cfg::SLICE_P;
@@ -137,7 +137,7 @@ __global__ void __launch_bounds__(DGR_THREADS, 1)
         }
         tc::named_bar_sync(1, NEPI);
         // task = (point pq, input il), input fastest: Xbar stores run along i
-        for (int task = etid; task < SLICE_P * n_in; task += NEPI) {
+        for (int task = etid; task < ((dbg & 4) ? 0 : SLICE_P * n_in); task += NEPI) {
           const int il = task % n_in, pq = task / n_in;
           const int pl = sl * SLICE_P + pq;
           const int64_t p = p0 + pl;

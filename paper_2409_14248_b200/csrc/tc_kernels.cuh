@@ -284,34 +284,40 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     // ===================== MMA issuer (one thread)
     if (lane == 0) {
       constexpr uint32_t idesc = tc::idesc_bf16(128, N);
+      // counters and descriptors advance incrementally (no integer division per K-block)
+      const uint32_t base = tc::smem_u32(smem);
+      const uint64_t bh0 = tc::smem_desc(base + Cfg::W_STAGE_BYTES, ACSB, 128);
+      const uint64_t bl0 = tc::smem_desc(base + Cfg::W_STAGE_BYTES + 2 * ACSB, ACSB, 128);
+      const uint64_t wh0 = tc::smem_desc(base, OP * 16, 128);
+      const uint64_t wl0 = tc::smem_desc(base + 2 * OP * 16, OP * 16, 128);
+      int s = 0, segc = 0, buf = 0, sgi = 0;
+      uint32_t ph = 0, use[2] = {0u, 0u};
       for (int kb = 0; kb < nkb; ++kb) {
-        const int sg = kb / seg, buf = sg % NACC;
-        const bool seg_first = (kb % seg) == 0;
-        if (seg_first && sg >= NACC) {
-          tc::mbar_wait(&acc_empty[buf], (uint32_t)((sg / NACC - 1) & 1));
+        const bool seg_first = segc == 0;
+        if (seg_first && sgi >= NACC) {
+          tc::mbar_wait(&acc_empty[buf], (use[buf] - 1) & 1);
           tc::tc_fence_after();
         }
-        const int s = kb % NSTAGE;
-        tc::mbar_wait(&full_bar[s], (kb / NSTAGE) & 1);
+        tc::mbar_wait(&full_bar[s], ph);
         tc::tc_fence_after();
-        const uint32_t w_hi = tc::smem_u32(smem + s * Cfg::STAGE_BYTES);
-        const uint32_t w_lo = w_hi + 2 * OP * 16;
-        const uint32_t a_hi = w_hi + Cfg::W_STAGE_BYTES;
-        const uint32_t a_lo = a_hi + 2 * ACSB;
-        // one K-step of 16 per stage: LBO = chunk stride, SBO = 8 rows = 128 B
-        const uint64_t bh = tc::smem_desc(a_hi, ACSB, 128);
-        const uint64_t bl = tc::smem_desc(a_lo, ACSB, 128);
+        const uint64_t off = (uint64_t)((uint32_t)(s * Cfg::STAGE_BYTES) >> 4);
 #pragma unroll
         for (int t = 0; t < NMT; ++t) {
-          const uint64_t wh = tc::smem_desc(w_hi + t * 128 * 16, OP * 16, 128);
-          const uint64_t wl = tc::smem_desc(w_lo + t * 128 * 16, OP * 16, 128);
+          const uint64_t toff = off + (uint64_t)((t * 128 * 16) >> 4);
           const uint32_t d = tmem + (uint32_t)((buf * NMT + t) * N);
-          tc::mma_bf16(d, wl, bh, idesc, seg_first ? 0u : 1u);
-          tc::mma_bf16(d, wh, bl, idesc, 1u);
-          tc::mma_bf16(d, wh, bh, idesc, 1u);
+          tc::mma_bf16(d, wl0 + toff, bh0 + off, idesc, seg_first ? 0u : 1u);
+          tc::mma_bf16(d, wh0 + toff, bl0 + off, idesc, 1u);
+          tc::mma_bf16(d, wh0 + toff, bh0 + off, idesc, 1u);
         }
         tc::mma_commit(&empty_bar[s]);
-        if ((kb % seg) == seg - 1 || kb == nkb - 1) tc::mma_commit(&acc_full[buf]);
+        if (++segc == seg || kb == nkb - 1) {
+          tc::mma_commit(&acc_full[buf]);
+          segc = 0;
+          ++use[buf];
+          ++sgi;
+          if (NACC == 2) buf ^= 1;
+        }
+        if (++s == NSTAGE) { s = 0; ph ^= 1u; }
       }
     }
     __syncwarp();
@@ -554,9 +560,11 @@ hrkan_status launch_wgrad_tc(hrkan_net* net, int l, const float* X, const float*
   float* part_b = part + (size_t)nslab * O * K;
   CUtensorMap tmX;
   HR_TRY(make_tmap_f32_3d(&tmX, X, (uint64_t)I, (uint64_t)C, (uint64_t)n, WGR_IW, C, WGR_JP));
-  HR_LAUNCH(HRKAN_K_WGRAD_HIDDEN, "k_wgrad_tc",
-            kfn<<<(unsigned)(nslab * nmt), WGR_THREADS, Cfg::SMEM_BYTES, st>>>(
-                tmX, (const uint16_t*)net->tc_yw.p, part, n, I, nmt, slab, net->tc_wseg, net->bc));
+  {
+    HR_LAUNCH(HRKAN_K_WGRAD_HIDDEN, "k_wgrad_tc",
+              kfn<<<(unsigned)(nslab * nmt), WGR_THREADS, Cfg::SMEM_BYTES, st>>>(
+                  tmX, (const uint16_t*)net->tc_yw.p, part, n, I, nmt, slab, net->tc_wseg, net->bc, net->tc_dbg));
+  }
   HR_LAUNCH(HRKAN_K_REDUCE, "k_reduce_slabs",
             k_reduce_slabs<<<(unsigned)((O * K + 255) / 256), 256, 0, st>>>(part, nslab, (int64_t)O * K, dW));
   const int nz = (int)std::min<int64_t>(1024, std::max<int64_t>(1, n / 256));
@@ -596,7 +604,7 @@ hrkan_status launch_dgrad_tc(hrkan_net* net, int l, const float* X, const float*
   const unsigned grid = (unsigned)((n + Cfg::NP - 1) / Cfg::NP);
   HR_LAUNCH(HRKAN_K_DGRAD_HIDDEN, "k_dgrad_tc",
             kfn<<<grid, DGR_THREADS, Cfg::SMEM_BYTES, st>>>(tmX, (const uint16_t*)net->tc_yd.p, ls.w_dgr, Xbar, n, I,
-                                                            128 / net->B, ls.ntile_dgr, net->bc));
+                                                            128 / net->B, ls.ntile_dgr, net->bc, net->tc_dbg));
   return HRKAN_OK;
 }
 
