@@ -201,6 +201,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--engine", type=int, default=0, help="0 auto, 1 SIMT only, 2 tensor cores")
     ap.add_argument("--chunk", type=int, default=0)
+    ap.add_argument("--graph", type=int, default=-1,
+                    help="CUDA-graph replay of the loss+grad call: 1 on, 0 off, -1 auto (on for the launch-bound C1/C2)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -283,7 +285,11 @@ def main():
     npar = net.n_params
     pde = pde_struct(w.pde, w.alpha, w.adv, w.visc)
     out = torch.empty(npar + 4, dtype=torch.float32, device=dev)
-    stream = torch.cuda.current_stream()
+    graph = (w.key in ("C1", "C2")) if args.graph < 0 else bool(args.graph)
+    # graph replay needs a non-legacy stream; eager runs use the current stream
+    stream = torch.cuda.Stream(device=dev) if graph else torch.cuda.current_stream()
+    torch.cuda.set_stream(stream)
+    net.set_graph_mode(graph)
 
     def step(i_int, i_bnd, i_gb, i_ini, i_gi, res=None):
         net.pinn_loss_grad(pde, i_int, i_bnd, i_gb, i_ini, i_gi, n_int_global=n_int_g, n_bi_global=n_bi_g, out=out)
@@ -293,7 +299,8 @@ def main():
         if res is not None:
             res.copy_(out[npar:npar + 4], non_blocking=True)
 
-    # warm-up (first warm-up step profiled per kernel class to find the dominant kernel)
+    # warm-up (first warm-up step profiled per kernel class to find the dominant kernel; with graph
+    # replay the per-launch events of that eager step are also the roofline measurement)
     net.profile_enable(True)
     for s in range(args.warmup):
         step(d_int, d_bnd, d_gb, d_ini, d_gi)
@@ -306,7 +313,7 @@ def main():
 
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # > 126 MB L2
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    net.profile_enable(True)            # live per-launch events for the kernel classes, same stream
+    net.profile_enable(not graph)       # live per-launch events for the kernel classes, same stream
     net.profile_read()
     launches0 = net.launch_count()
     if world > 1:
@@ -324,6 +331,9 @@ def main():
     launches = net.launch_count() - launches0
     prof = net.profile_read()
     net.profile_enable(False)
+    prof_steps = args.steps
+    if graph:                            # per-class device times of the profiled eager warm-up step
+        prof, prof_steps = prof0, 1
     ms = sum(a.elapsed_time(b) for a, b in ev) / args.steps
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
@@ -365,9 +375,9 @@ def main():
     c_int = interior_channels(w)
     fl = class_flops(w, len(sh.interior), sh.n_bi, c_int)
     dom_ms, dom_n = prof[dominant]
-    dom_flops = fl.get(dominant, 0) * args.steps
+    dom_flops = fl.get(dominant, 0) * prof_steps
     step_ms_local = ms
-    share = (dom_ms / args.steps) / step_ms_local if step_ms_local > 0 else None
+    share = (dom_ms / prof_steps) / step_ms_local if step_ms_local > 0 else None
     clock_mhz = pk["sm_max_mhz"]
     # SIMT (FFMA) peak = 148 SMs x 128 FP32 lanes x 2 flop x SM clock; TF32 tensor = bf16 x (1.1/2.25)
     n_sms = torch.cuda.get_device_properties(dev).multi_processor_count
@@ -386,7 +396,8 @@ def main():
                               else f"BF16 dense sustained {pk['bf16_sustained']} TFLOP/s ({pk['source']} peak); "
                                    f"achieved counts fp32-equivalent algorithmic FLOPs, bf16x3 issues 3 MMAs per "
                                    f"product, so frac <= 1/3"),
-                "per_class_ms_per_step": {k: v[0] / args.steps for k, v in prof.items() if v[1]}}
+                "per_class_ms_per_step": {k: v[0] / prof_steps for k, v in prof.items() if v[1]},
+                "events": "live, timed region" if not graph else "eager profiled warm-up step (timed steps are graph replays)"}
 
     if rank == 0:
         cpu = None
@@ -400,7 +411,7 @@ def main():
                 "config": {"workload": w.key, "name": w.name, "n_interior": n_int_g, "n_boundary_initial": n_bi_g,
                            "widths": list(w.widths), "G": w.G, "k": w.k, "m": w.m, "pde": w.pde,
                            "parallelism": f"dp{world}", "l2": "flushed between timed steps (256 MiB write)",
-                           "engine": args.engine},
+                           "engine": args.engine, "cuda_graph": graph},
                 "e2e": e2e, "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpu,
                 "clocks": clk.summary(), "loss": loss, "nonfinite_flag": flag,
                 "step": "pinn_loss_grad + allreduce(N>1) + adam_step"}

@@ -133,6 +133,16 @@ hrkan_status hrkan_set_chunk_points(hrkan_net_t net, int64_t chunk);
  * EINVAL: unknown mode. */
 hrkan_status hrkan_set_engine(hrkan_net_t net, int32_t mode);
 
+/* CUDA-graph replay of hrkan_pinn_loss_grad (enable != 0).  When enabled, and the call uses only
+ * device buffers on a non-legacy stream that is not already being captured, and per-launch profiling
+ * is off: the first call with a given argument signature (all pointers, counts, pde fields, stream,
+ * chunk size, engine) runs eagerly, the second captures the whole call into a CUDA graph (weight
+ * re-tiling included) and later calls replay it with one cudaGraphLaunch -- the launch-latency
+ * bound small configs (C1, C2) become one graph launch per step.  Results are bitwise identical to
+ * eager calls.  Changing any argument re-captures.  A caller's own stream capture (e.g. of a whole
+ * training step with the NCCL allreduce) simply records the eager launches.  EINVAL: net == NULL. */
+hrkan_status hrkan_set_graph_mode(hrkan_net_t net, int32_t enable);
+
 /* Number of kernels the library launched on this net since creation (for bench accounting). */
 int64_t hrkan_launch_count(hrkan_net_t net);
 

@@ -25,8 +25,8 @@ void clear_error() { g_err.clear(); }
 
 namespace {
 
-hrkan_status refresh_derived(hrkan_net* net, cudaStream_t st) {
-  if (!net->derived_dirty) return HRKAN_OK;
+hrkan_status refresh_derived(hrkan_net* net, cudaStream_t st, bool force = false) {
+  if (!net->derived_dirty && !force) return HRKAN_OK;
   for (int l = 0; l < net->L; ++l) {
     const int I = net->widths[l], O = net->widths[l + 1];
     const int64_t n = (int64_t)O * I * net->B;
@@ -246,23 +246,15 @@ hrkan_status hrkan_forward_jet(hrkan_net_t net, const float* pts, int64_t P, flo
   return HRKAN_OK;
 }
 
-hrkan_status hrkan_pinn_loss_grad(hrkan_net_t net, const hrkan_pde* pde, const float* interior, const float* forcing,
-                                  int64_t Ni, const float* boundary, const float* g_boundary, int64_t Nb,
-                                  const float* initial, const float* g_initial, int64_t N0, int64_t Ni_global,
-                                  int64_t Nbi_global, float* out, void* stream) {
-  if (!net) return fail(HRKAN_EINVAL, "net is NULL");
-  if (!pde) return fail(HRKAN_EINVAL, "pde is NULL");
-  if (!out) return fail(HRKAN_EINVAL, "out is NULL");
-  if (Ni < 0 || Nb < 0 || N0 < 0) return fail(HRKAN_EINVAL, "negative point count");
-  if ((Ni > 0 && !interior) || (Nb > 0 && (!boundary || !g_boundary)) || (N0 > 0 && (!initial || !g_initial)))
-    return fail(HRKAN_EINVAL, "NULL point/target buffer with a non-zero count");
-  if (Ni_global < Ni || Nbi_global < Nb + N0) return fail(HRKAN_EINVAL, "global normalisers smaller than local counts");
-  if (pde->kind != HRKAN_POISSON && pde->kind != HRKAN_BURGERS) return fail(HRKAN_EINVAL, "unknown pde kind");
-  if (pde->kind == HRKAN_BURGERS && net->D != 2) return fail(HRKAN_EINVAL, "Burgers needs D = 2 (x, t)");
-  if (!std::isfinite(pde->alpha)) return fail(HRKAN_EINVAL, "alpha must be finite");
-  clear_error();
-  DeviceGuard dg(net->device);
-  cudaStream_t st = (cudaStream_t)stream;
+}  // extern "C"
+
+namespace {
+
+// The work of hrkan_pinn_loss_grad after argument validation (stream-ordered launches only).
+hrkan_status loss_grad_body(hrkan_net* net, const hrkan_pde* pde, const float* interior, const float* forcing,
+                            int64_t Ni, const float* boundary, const float* g_boundary, int64_t Nb,
+                            const float* initial, const float* g_initial, int64_t N0, int64_t Ni_global,
+                            int64_t Nbi_global, float* out, cudaStream_t st, bool force_refresh) {
   const int D = net->D;
   const int64_t np = net->n_params;
   const float *d_int, *d_f = nullptr, *d_bnd, *d_gb, *d_ini, *d_gi;
@@ -279,7 +271,7 @@ hrkan_status hrkan_pinn_loss_grad(hrkan_net_t net, const hrkan_pde* pde, const f
     dout = net->st_out.f();
   }
   HR_CUDA(cudaMemsetAsync(dout, 0, sizeof(float) * (np + 4), st));
-  HR_TRY(refresh_derived(net, st));
+  HR_TRY(refresh_derived(net, st, force_refresh));
   PassArgs a{};
   a.grad = dout;
   a.pde = pde;
@@ -311,6 +303,105 @@ hrkan_status hrkan_pinn_loss_grad(hrkan_net_t net, const hrkan_pde* pde, const f
     HR_TRY(dispatch_pass(net, 0, 0, a, st));
   }
   if (host_out) HR_CUDA(cudaMemcpyAsync(out, dout, sizeof(float) * (np + 4), cudaMemcpyDeviceToHost, st));
+  return HRKAN_OK;
+}
+
+
+bool same_key(const GraphKey& a, const GraphKey& b) { return std::memcmp(&a, &b, sizeof(GraphKey)) == 0; }
+
+}  // namespace
+
+extern "C" {
+
+hrkan_status hrkan_pinn_loss_grad(hrkan_net_t net, const hrkan_pde* pde, const float* interior, const float* forcing,
+                                  int64_t Ni, const float* boundary, const float* g_boundary, int64_t Nb,
+                                  const float* initial, const float* g_initial, int64_t N0, int64_t Ni_global,
+                                  int64_t Nbi_global, float* out, void* stream) {
+  if (!net) return fail(HRKAN_EINVAL, "net is NULL");
+  if (!pde) return fail(HRKAN_EINVAL, "pde is NULL");
+  if (!out) return fail(HRKAN_EINVAL, "out is NULL");
+  if (Ni < 0 || Nb < 0 || N0 < 0) return fail(HRKAN_EINVAL, "negative point count");
+  if ((Ni > 0 && !interior) || (Nb > 0 && (!boundary || !g_boundary)) || (N0 > 0 && (!initial || !g_initial)))
+    return fail(HRKAN_EINVAL, "NULL point/target buffer with a non-zero count");
+  if (Ni_global < Ni || Nbi_global < Nb + N0) return fail(HRKAN_EINVAL, "global normalisers smaller than local counts");
+  if (pde->kind != HRKAN_POISSON && pde->kind != HRKAN_BURGERS) return fail(HRKAN_EINVAL, "unknown pde kind");
+  if (pde->kind == HRKAN_BURGERS && net->D != 2) return fail(HRKAN_EINVAL, "Burgers needs D = 2 (x, t)");
+  if (!std::isfinite(pde->alpha)) return fail(HRKAN_EINVAL, "alpha must be finite");
+  clear_error();
+  DeviceGuard dg(net->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  // CUDA-graph replay (hrkan_set_graph_mode): device buffers only, non-legacy stream, not already
+  // inside a caller's capture, no per-launch profiling.  The first call with a new argument
+  // signature runs eagerly (allocating every workspace), the second captures the whole call
+  // (weight re-tiling included, since Adam changes the parameters between calls) and every later
+  // call replays it with one cudaGraphLaunch.
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  bool graph_ok = net->graph_mode && !net->prof_on && st != nullptr &&
+                  cudaStreamIsCapturing(st, &cap) == cudaSuccess && cap == cudaStreamCaptureStatusNone;
+  if (graph_ok) {
+    const void* ptrs[] = {interior, forcing, boundary, g_boundary, initial, g_initial, out};
+    for (const void* q : ptrs) graph_ok = graph_ok && is_device_ptr(q);
+  }
+  cudaGetLastError();
+  if (!graph_ok)
+    return loss_grad_body(net, pde, interior, forcing, Ni, boundary, g_boundary, Nb, initial, g_initial, N0, Ni_global,
+                          Nbi_global, out, st, false);
+  GraphKey key;
+  std::memset(&key, 0, sizeof(key));
+  const void* kp[] = {interior, forcing, boundary, g_boundary, initial, g_initial, out, st};
+  std::memcpy(key.ptrs, kp, sizeof(kp));
+  key.n[0] = Ni; key.n[1] = Nb; key.n[2] = N0; key.n[3] = Ni_global; key.n[4] = Nbi_global; key.n[5] = net->chunk;
+  key.kind = pde->kind; key.engine = net->engine;
+  key.f[0] = pde->alpha; key.f[1] = pde->adv; key.f[2] = pde->visc;
+  if (net->graph_exec && same_key(key, net->graph_key)) {
+    HR_CUDA(cudaGraphLaunch(net->graph_exec, st));
+    net->launches += net->graph_launches;
+    net->derived_dirty = false;
+    return HRKAN_OK;
+  }
+  if (!same_key(key, net->graph_key)) {           // new signature: run eagerly, capture next time
+    if (net->graph_exec) cudaGraphExecDestroy(net->graph_exec);
+    net->graph_exec = nullptr;
+    net->graph_key = key;
+    return loss_grad_body(net, pde, interior, forcing, Ni, boundary, g_boundary, Nb, initial, g_initial, N0, Ni_global,
+                          Nbi_global, out, st, false);
+  }
+  const int64_t l0 = net->launches;
+  HR_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+  const hrkan_status sb = loss_grad_body(net, pde, interior, forcing, Ni, boundary, g_boundary, Nb, initial, g_initial,
+                                         N0, Ni_global, Nbi_global, out, st, true);
+  cudaGraph_t graph = nullptr;
+  const cudaError_t ec = cudaStreamEndCapture(st, &graph);
+  net->graph_launches = net->launches - l0;
+  net->launches = l0;
+  if (sb != HRKAN_OK || ec != cudaSuccess || !graph) {
+    if (graph) cudaGraphDestroy(graph);
+    cudaGetLastError();
+    std::memset(&net->graph_key, 0, sizeof(GraphKey));
+    if (sb != HRKAN_OK) return sb;
+    return fail(HRKAN_ECUDA, std::string("graph capture failed: ") + cudaGetErrorString(ec));
+  }
+  const cudaError_t ei = cudaGraphInstantiate(&net->graph_exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (ei != cudaSuccess) {
+    net->graph_exec = nullptr;
+    std::memset(&net->graph_key, 0, sizeof(GraphKey));
+    return fail(HRKAN_ECUDA, std::string("cudaGraphInstantiate: ") + cudaGetErrorString(ei));
+  }
+  HR_CUDA(cudaGraphLaunch(net->graph_exec, st));
+  net->launches += net->graph_launches;
+  net->derived_dirty = false;
+  return HRKAN_OK;
+}
+
+hrkan_status hrkan_set_graph_mode(hrkan_net_t net, int32_t enable) {
+  if (!net) return fail(HRKAN_EINVAL, "net is NULL");
+  net->graph_mode = enable != 0;
+  if (!net->graph_mode && net->graph_exec) {
+    cudaGraphExecDestroy(net->graph_exec);
+    net->graph_exec = nullptr;
+  }
+  std::memset(&net->graph_key, 0, sizeof(GraphKey));
   return HRKAN_OK;
 }
 
@@ -365,6 +456,7 @@ void hrkan_free(hrkan_net_t net) {
   if (!net) return;
   DeviceGuard dg(net->device);
   cudaDeviceSynchronize();
+  if (net->graph_exec) cudaGraphExecDestroy(net->graph_exec);
   for (auto& ev : net->prof_pool) {
     cudaEventDestroy(ev.a);
     cudaEventDestroy(ev.b);

@@ -97,6 +97,14 @@ struct TcLayerState {
 
 using namespace hrkan;
 
+// Argument signature of a captured hrkan_pinn_loss_grad call (CUDA-graph replay).
+struct GraphKey {
+  const void* ptrs[8];
+  int64_t n[6];
+  float f[3];
+  int32_t kind, engine;
+};
+
 struct hrkan_net {
   int device = 0;
   int L = 0, D = 0, G = 0, k = 0, m = 0, B = 0;
@@ -126,6 +134,11 @@ struct hrkan_net {
   int tc_seg = 32;                      // K-blocks per TMEM accumulation segment (precision bound)
   int tc_wseg = 256;                    // wgrad stages per TMEM drain into the fp32 master
   int tc_dbg = 0;                       // timing-experiment switches (HRKAN_TC_DBG; 0 in production)
+  // CUDA-graph replay of hrkan_pinn_loss_grad (hrkan_set_graph_mode)
+  bool graph_mode = false;
+  GraphKey graph_key{};
+  cudaGraphExec_t graph_exec = nullptr;
+  int64_t graph_launches = 0;
   // device-time profiling (hrkan_profile_enable / hrkan_profile_read)
   struct ProfEv { cudaEvent_t a, b; int cls; };
   bool prof_on = false;

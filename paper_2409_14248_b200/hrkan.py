@@ -39,6 +39,7 @@ SYMBOLS = [
     ("hrkan_adam_step", ctypes.c_int, [_P, _P, _F, _F, _F, _F, _P]),
     ("hrkan_set_chunk_points", ctypes.c_int, [_P, _I64]),
     ("hrkan_set_engine", ctypes.c_int, [_P, _I32]),
+    ("hrkan_set_graph_mode", ctypes.c_int, [_P, _I32]),
     ("hrkan_launch_count", _I64, [_P]),
     ("hrkan_profile_enable", ctypes.c_int, [_P, _I32]),
     ("hrkan_profile_read", ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_I64)]),
@@ -165,6 +166,10 @@ class HRKANNet:
 
     def set_engine(self, mode: int):
         _check(_lib.hrkan_set_engine(self._h, mode), "hrkan_set_engine")
+
+    def set_graph_mode(self, on: bool = True):
+        """CUDA-graph replay of pinn_loss_grad for repeated calls with the same device buffers."""
+        _check(_lib.hrkan_set_graph_mode(self._h, 1 if on else 0), "hrkan_set_graph_mode")
 
     def launch_count(self) -> int:
         return int(_lib.hrkan_launch_count(self._h))

@@ -199,6 +199,34 @@ def test_determinism_and_chunk_invariance(torch_mod):
     assert rel_l2(c, a) < 1e-5
 
 
+@pytest.mark.parametrize("key", ["C2", "C5"])
+def test_graph_replay_matches_eager(torch_mod, key):
+    """hrkan_set_graph_mode: eager call, capture, replays -- with Adam steps in between (the graph
+    re-tiles the changing weights) -- bitwise equal to a twin net run eagerly."""
+    torch = torch_mod
+    from paper_2409_14248_b200 import pde_struct
+    w = HI.WORKLOADS[key]
+    ps = HI.make_points(w) if key == "C2" else HI.make_points(w).subset(4096, 64)
+    cu = lambda a: None if a is None else torch.from_numpy(a).cuda()
+    args = [cu(ps.interior), cu(ps.boundary), cu(ps.g_boundary), cu(ps.initial), cu(ps.g_initial)]
+    pde = pde_struct(w.pde, w.alpha, w.adv, w.visc)
+    s = torch.cuda.Stream()
+    outs = []
+    for graph in (False, True):
+        net, _ = _make(w, chunk=1500)
+        net.set_graph_mode(graph)
+        out = torch.empty(w.num_params() + 4, device="cuda")
+        res = []
+        with torch.cuda.stream(s):
+            for it in range(4):
+                net.pinn_loss_grad(pde, *args, out=out)
+                res.append(out.clone())
+                net.adam_step(out[:w.num_params()], lr=1e-3)
+        torch.cuda.synchronize()
+        outs.append(torch.stack(res).cpu().numpy())
+    np.testing.assert_array_equal(outs[0], outs[1])
+
+
 def test_fake_collective_shards_sum(torch_mod):
     """Shards evaluated one after another with global normalisers sum to the unsharded call."""
     torch = torch_mod
