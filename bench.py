@@ -69,6 +69,7 @@ def class_flops(w: HI.Workload, n_int: int, n_bi: int, c_int: int):
                 tot += n * per
             key = f"{cls}_{kind}"
             out[key] = out.get(key, 0) + tot
+    out["fused_step"] = sum(out.values())      # the one-launch tiny-net kernel does every layer
     return out
 
 

@@ -128,8 +128,9 @@ hrkan_status hrkan_adam_step(hrkan_net_t net, const float* grad, float lr, float
  * workspace, SURVEY §7 hard part (f)).  0 = default.  EINVAL: chunk < 0. */
 hrkan_status hrkan_set_chunk_points(hrkan_net_t net, int64_t chunk);
 
-/* Select the hidden-layer contraction engine: 0 = auto (tensor-core tcgen05 path where the layer
- * is wide, SIMT FFMA otherwise), 1 = force SIMT FFMA kernels, 2 = force tcgen05 where supported.
+/* Select the engine: 0 = auto (one-launch fused kernel for tiny nets -- every width <= 8, <= 4 layers
+ * -- else tcgen05 tensor cores where a hidden layer is wide and SIMT FFMA elsewhere), 1 = force the
+ * layered SIMT FFMA kernels, 2 = force tcgen05 where supported (layered).
  * EINVAL: unknown mode. */
 hrkan_status hrkan_set_engine(hrkan_net_t net, int32_t mode);
 
@@ -151,7 +152,8 @@ typedef enum {
   HRKAN_K_FWD_FIRST = 0, HRKAN_K_FWD_HIDDEN = 1, HRKAN_K_FWD_LAST = 2, HRKAN_K_LOSS = 3,
   HRKAN_K_WGRAD_FIRST = 4, HRKAN_K_WGRAD_HIDDEN = 5, HRKAN_K_WGRAD_LAST = 6,
   HRKAN_K_DGRAD_HIDDEN = 7, HRKAN_K_DGRAD_LAST = 8, HRKAN_K_REDUCE = 9, HRKAN_K_ADAM = 10,
-  HRKAN_K_OTHER = 11, HRKAN_K_NUM_CLASSES = 12
+  HRKAN_K_OTHER = 11, HRKAN_K_FUSED_STEP = 12 /* one-launch tiny-net loss+grad (all layers) */,
+  HRKAN_K_NUM_CLASSES = 13
 } hrkan_kernel_class;
 
 /* Device-time profiling: while enabled, every launch is bracketed by CUDA events recorded on the

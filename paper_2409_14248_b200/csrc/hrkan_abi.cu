@@ -51,6 +51,27 @@ hrkan_status stage_in(const float* src, int64_t n, DevBuf& buf, cudaStream_t st,
 }
 
 
+hrkan_status tiny_step(hrkan_net* net, const TinyArgs& t, cudaStream_t st) {
+  switch (net->m) {
+    case 2: return tiny_step_m2(net, t, st);
+    case 3: return tiny_step_m3(net, t, st);
+    case 4: return tiny_step_m4(net, t, st);
+    case 5: return tiny_step_m5(net, t, st);
+    case 6: return tiny_step_m6(net, t, st);
+    case 7: return tiny_step_m7(net, t, st);
+    case 8: return tiny_step_m8(net, t, st);
+  }
+  return fail(HRKAN_EINVAL, "m must be in [2, 8]");
+}
+
+// The one-launch tiny-net step applies: every width <= 8, <= 4 layers, few parameters.
+bool tiny_eligible(const hrkan_net* net) {
+  if (net->engine != 0 || net->L > 4 || net->n_params > 2048 || net->k + 1 > KMAX) return false;
+  for (int w : net->widths)
+    if (w > 8) return false;
+  return true;
+}
+
 hrkan_status dispatch_pass(hrkan_net* net, int nf, int ns, const PassArgs& a, cudaStream_t st) {
   switch (net->m) {
     case 2: return dispatch_pass_m2(net, nf, ns, a, st);
@@ -269,6 +290,13 @@ hrkan_status loss_grad_body(hrkan_net* net, const hrkan_pde* pde, const float* i
   if (host_out) {
     HR_CUDA(net->st_out.ensure(sizeof(float) * (np + 4)));
     dout = net->st_out.f();
+  }
+  if (tiny_eligible(net)) {
+    TinyArgs t{pde, d_int, d_f, d_bnd, d_gb, d_ini, d_gi, Ni, Nb, N0, (float)(1.0 / (double)std::max<int64_t>(1, Ni_global)),
+               Nbi_global > 0 ? (float)(1.0 / (double)Nbi_global) : 0.f, dout};
+    HR_TRY(tiny_step(net, t, st));
+    if (host_out) HR_CUDA(cudaMemcpyAsync(out, dout, sizeof(float) * (np + 4), cudaMemcpyDeviceToHost, st));
+    return HRKAN_OK;
   }
   HR_CUDA(cudaMemsetAsync(dout, 0, sizeof(float) * (np + 4), st));
   HR_TRY(refresh_derived(net, st, force_refresh));

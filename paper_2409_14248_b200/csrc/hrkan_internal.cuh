@@ -265,9 +265,19 @@ struct PassArgs {
 
 // Forward + (optional) loss/seeds + reverse over one point set, chunk by chunk.
 
+// Arguments of the one-launch tiny-net step (tiny_kernels.cuh); device pointers.
+struct TinyArgs {
+  const hrkan_pde* pde;
+  const float *interior, *forcing, *boundary, *g_boundary, *initial, *g_initial;
+  int64_t Ni, Nb, N0;
+  float inv_int, inv_bi;
+  float* out;
+};
+
 // One scheduler per HR order m (pass_m<m>.cu).
 #define HRKAN_DECLARE_DISPATCH(MM) \
-  hrkan_status dispatch_pass_m##MM(hrkan_net* net, int nf, int ns, const PassArgs& a, cudaStream_t st);
+  hrkan_status dispatch_pass_m##MM(hrkan_net* net, int nf, int ns, const PassArgs& a, cudaStream_t st); \
+  hrkan_status tiny_step_m##MM(hrkan_net* net, const TinyArgs& t, cudaStream_t st);
 HRKAN_DECLARE_DISPATCH(2)
 HRKAN_DECLARE_DISPATCH(3)
 HRKAN_DECLARE_DISPATCH(4)

@@ -6,6 +6,7 @@
 #include "simt_kernels.cuh"
 #include "last_kernels.cuh"
 #include "first_kernels.cuh"
+#include "tiny_kernels.cuh"
 #include "tc_kernels.cuh"
 
 namespace {
@@ -221,11 +222,52 @@ hrkan_status with_channels(int nf, int ns, F&& f) {
 
 }  // namespace
 
+// Whole loss + gradient of a tiny net in one launch (+ one reduction launch), tiny_kernels.cuh.
+template <int M>
+hrkan_status run_tiny(hrkan_net* net, const TinyArgs& t, cudaStream_t st) {
+  TinyNet tn{};
+  tn.L = net->L;
+  tn.B = net->B;
+  tn.np = (int)net->n_params;
+  for (int l = 0; l <= net->L; ++l) tn.w[l] = net->widths[l];
+  for (int l = 0; l < net->L; ++l) {
+    tn.woff[l] = (int)net->w_off[l];
+    tn.boff[l] = (int)net->b_off[l];
+  }
+  const int nb_int = (int)((t.Ni + TINY_THREADS - 1) / TINY_THREADS);
+  const int nb_bnd = (int)((t.Nb + TINY_THREADS - 1) / TINY_THREADS);
+  const int nb_ini = (int)((t.N0 + TINY_THREADS - 1) / TINY_THREADS);
+  const int nb = std::max(1, nb_int + nb_bnd + nb_ini);
+  HR_CUDA(net->last_part.ensure(sizeof(float) * (size_t)nb * (tn.np + 4)));
+  const hrkan_pde* pde = t.pde;
+  auto go = [&](auto NFc, auto NSc, auto BUR) -> hrkan_status {
+    constexpr int NF = decltype(NFc)::value, NS = decltype(NSc)::value;
+    constexpr bool BURGERS = decltype(BUR)::value;
+    HR_LAUNCH(HRKAN_K_FUSED_STEP, "k_tiny_step",
+              (k_tiny_step<NF, NS, M, BURGERS><<<nb, TINY_THREADS, 0, st>>>(
+                  tn, net->params, net->bc, net->D, t.interior, t.forcing, t.Ni, nb_int, t.boundary, t.g_boundary, t.Nb,
+                  nb_bnd, t.initial, t.g_initial, t.N0, pde->alpha, pde->adv, pde->visc, t.inv_int, t.inv_bi,
+                  net->last_part.f())));
+    return HRKAN_OK;
+  };
+  if (pde->kind == HRKAN_BURGERS) HR_TRY(go(IC<2>{}, IC<1>{}, std::true_type{}));
+  else if (net->D == 1) HR_TRY(go(IC<1>{}, IC<1>{}, std::false_type{}));
+  else if (net->D == 2) HR_TRY(go(IC<2>{}, IC<2>{}, std::false_type{}));
+  else HR_TRY(go(IC<3>{}, IC<3>{}, std::false_type{}));
+  HR_LAUNCH(HRKAN_K_REDUCE, "k_tiny_reduce",
+            k_tiny_reduce<<<(tn.np + 4 + 255) / 256, 256, 0, st>>>(net->last_part.f(), nb, tn.np,
+                                                                   pde->alpha * t.inv_int, t.inv_bi, t.out));
+  return HRKAN_OK;
+}
+
 #define HRKAN_DEFINE_DISPATCH(MM)                                                                   \
   namespace hrkan {                                                                                \
   hrkan_status dispatch_pass_m##MM(hrkan_net* net, int nf, int ns, const PassArgs& a, cudaStream_t st) { \
     return with_channels(nf, ns, [&](auto NFc, auto NSc) {                                        \
       return run_pass<decltype(NFc)::value, decltype(NSc)::value, MM>(net, a, st);                \
     });                                                                                            \
+  }                                                                                                \
+  hrkan_status tiny_step_m##MM(hrkan_net* net, const TinyArgs& t, cudaStream_t st) {             \
+    return run_tiny<MM>(net, t, st);                                                               \
   }                                                                                                \
   }

@@ -21,7 +21,7 @@ HRKAN_BURGERS = 1
 ENGINE_AUTO, ENGINE_SIMT, ENGINE_TC = 0, 1, 2
 
 KERNEL_CLASSES = ["fwd_first", "fwd_hidden", "fwd_last", "loss", "wgrad_first", "wgrad_hidden", "wgrad_last",
-                  "dgrad_hidden", "dgrad_last", "reduce", "adam", "other"]   # hrkan_kernel_class order
+                  "dgrad_hidden", "dgrad_last", "reduce", "adam", "other", "fused_step"]   # hrkan_kernel_class order
 
 _STATUS = {0: "OK", 1: "EINVAL", 2: "EUNSUPPORTED", 3: "ENOMEM", 4: "ECUDA", 5: "ENONFINITE"}
 

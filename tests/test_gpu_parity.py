@@ -118,6 +118,21 @@ def test_loss_grad_parity(torch_mod, w):
     _check_loss_grad(out, w, lp, lb, g)
 
 
+@pytest.mark.parametrize("key", ["C1", "C2"])
+def test_tiny_fused_step_matches_layered(torch_mod, key):
+    """The one-launch tiny-net kernel (engine auto for widths <= 8) agrees with the layered SIMT
+    kernels (engine 1): same formulas, different summation order."""
+    torch = torch_mod
+    w = HI.WORKLOADS[key]
+    ps = HI.make_points(w)
+    outs = []
+    for engine in (0, 1):
+        net, _ = _make(w, engine=engine)
+        outs.append(_loss_grad_gpu(torch, net, w, ps))
+    assert rel_l2(outs[0][:-4], outs[1][:-4]) < 1e-5
+    np.testing.assert_allclose(outs[0][-4:-2], outs[1][-4:-2], rtol=1e-5)
+
+
 def test_loss_grad_parity_simt_engine_c3(torch_mod):
     """The SIMT engine alone (the reference engine for every tensor-core kernel)."""
     torch = torch_mod
