@@ -44,8 +44,8 @@ struct DgrCfg {
   static_assert(STAGE_BYTES % 128 == 0, "TMA boxes after the stages need 128-B alignment");
 };
 constexpr int DGR_EPI_WARPS = 8;       // two epilogue warps per TMEM lane quadrant
-constexpr int DGR_THREADS = 32 * (DGR_EPI_WARPS + 2);   // + MMA warp + producer warp
-constexpr int DGR_MMA_WARP = DGR_EPI_WARPS, DGR_PROD_WARP = DGR_EPI_WARPS + 1;
+constexpr int DGR_THREADS = 32 * (DGR_EPI_WARPS + 3);   // + MMA warp + stage producer + jet producer
+constexpr int DGR_MMA_WARP = DGR_EPI_WARPS, DGR_PROD_WARP = DGR_EPI_WARPS + 1, DGR_JET_WARP = DGR_EPI_WARPS + 2;
 
 // W^T tiles for k_dgrad_tc: for M-tile mt (inputs mt*IPT ...), K-block kb (o = kb*KB ...):
 // [hi | lo] each [2 chunks][128 rows][8] bf16, row = il*B + n (il < IPT), zero outside.
@@ -224,19 +224,13 @@ __global__ void __launch_bounds__(DGR_THREADS, 1)
       }
     }
     __syncwarp();
-  } else {
-    // ===================== producer: W^T and pre-split Ybar stages (1-D bulk copies), jet boxes (TMA)
+  } else if (warp == DGR_PROD_WARP) {
+    // ===================== producer: W^T and pre-split Ybar stages (1-D bulk copies); never waits on the
+    // epilogue, so the MMA is only held back by the TMEM accumulators it releases early
     if (lane == 0) {
-      tc::tma_prefetch_desc(&tmX);
       const uint16_t* ytile = Ysplit + (int64_t)blockIdx.x * NKB * (Cfg::Y_STAGE_BYTES / 2);
       for (int g = 0; g < nblk; ++g) {
-        const int mt = g / NKB, kb = g - (g / NKB) * NKB;
-        if (kb == 0) {
-          const int jb = mt & 1;
-          if (mt >= 2) tc::mbar_wait(&jet_empty[jb], (uint32_t)(((mt >> 1) - 1) & 1));
-          tc::mbar_arrive_expect_tx(&jet_full[jb], Cfg::JET_FLOATS * 4);
-          tc::tma_load_3d(jets + jb * Cfg::JET_FLOATS, &tmX, (mt * IPT) & ~3, 0, (int)p0, &jet_full[jb]);
-        }
+        const int kb = g - (g / NKB) * NKB;
         const int s = g % NSTAGE;
         tc::mbar_wait(&empty_bar[s], ((g / NSTAGE) & 1) ^ 1);
         tc::mbar_arrive_expect_tx(&full_bar[s], Cfg::STAGE_BYTES);
@@ -244,6 +238,18 @@ __global__ void __launch_bounds__(DGR_THREADS, 1)
                      &full_bar[s]);
         tc::bulk_g2s(smem + s * Cfg::STAGE_BYTES + Cfg::W_STAGE_BYTES, ytile + (int64_t)kb * (Cfg::Y_STAGE_BYTES / 2),
                      Cfg::Y_STAGE_BYTES, &full_bar[s]);
+      }
+    }
+    __syncwarp();
+  } else {
+    // ===================== jet producer: input-jet boxes of the M-tiles (TMA), two tiles ahead of use
+    if (lane == 0) {
+      tc::tma_prefetch_desc(&tmX);
+      for (int mt = 0; mt < nmt; ++mt) {
+        const int jb = mt & 1;
+        if (mt >= 2) tc::mbar_wait(&jet_empty[jb], (uint32_t)(((mt >> 1) - 1) & 1));
+        tc::mbar_arrive_expect_tx(&jet_full[jb], Cfg::JET_FLOATS * 4);
+        tc::tma_load_3d(jets + jb * Cfg::JET_FLOATS, &tmX, (mt * IPT) & ~3, 0, (int)p0, &jet_full[jb]);
       }
     }
     __syncwarp();
