@@ -86,9 +86,14 @@ __global__ void __launch_bounds__(FL_THREADS) k_fwd_first(const float* __restric
     }
     __syncthreads();
     const int nq = (int)((P - p0) < FL_BATCH ? (P - p0) : FL_BATCH);
-    for (int o = threadIdx.x; o < O; o += blockDim.x) {
+    // thread -> (output o, point group qg): narrow layers (O < blockDim) split the batch's points
+    const int QG = O <= (int)blockDim.x ? (int)blockDim.x / O : 1;
+    const int qg = O <= (int)blockDim.x ? (int)threadIdx.x / O : 0;
+    const int o0 = (O <= (int)blockDim.x && qg >= QG) ? O : (O <= (int)blockDim.x ? (int)threadIdx.x % O : (int)threadIdx.x);
+    const int ostep = O <= (int)blockDim.x ? O : (int)blockDim.x;
+    for (int o = o0; o < O; o += ostep) {
       const float b = __ldg(bias + o);
-      for (int q = 0; q < nq; ++q) {
+      for (int q = qg; q < nq; q += QG) {
         float acc[C];
         acc[0] = b;
 #pragma unroll
@@ -122,9 +127,11 @@ __global__ void __launch_bounds__(FL_THREADS) k_fwd_first(const float* __restric
   }
 }
 
-// Weight gradient of the first layer: a grid of blocks over contiguous point ranges; thread o keeps
-// its (a, n) accumulators in shared memory acc[a][n][o] (private column, no atomics); the block writes
-// part[block][O][D][B] (+ part_b[block][O]) and k_reduce_parts sums the blocks in a fixed order.
+// Weight gradient of the first layer: a grid of blocks over contiguous point ranges; thread (o, point
+// group qg) keeps its (a, n) accumulators in shared memory acc[qg][a][n][o] (private column, no
+// atomics); the block sums its point groups in a fixed order into part[block][O][D][B] (+ part_b)
+// and k_reduce_parts sums the blocks in a fixed order.  Narrow layers (O < blockDim) use several
+// point groups so that every thread works.
 template <int NF, int NS, int M>
 __global__ void __launch_bounds__(FL_THREADS) k_wgrad_first(const float* __restrict__ pts,
                                                             const float* __restrict__ Ybar, float* __restrict__ part,
@@ -133,10 +140,18 @@ __global__ void __launch_bounds__(FL_THREADS) k_wgrad_first(const float* __restr
   constexpr int D = (NF > 0) ? NF : 1;
   constexpr int C = 1 + NF + NS;
   __shared__ FlBasis tab[FL_BATCH * 3];
-  extern __shared__ float acc[];          // [Dr][B][O]
+  __shared__ float dbs_sh[FL_THREADS * 2];
+  extern __shared__ float acc[];          // [QG][Dr][B][O]
   const int Dr = (NF > 0) ? D : D_;
   const int B = bc.B;
-  for (int e = threadIdx.x; e < Dr * B * O; e += blockDim.x) acc[e] = 0.f;
+  const int QG = O <= (int)blockDim.x ? (int)blockDim.x / O : 1;
+  const int qg = O <= (int)blockDim.x ? (int)threadIdx.x / O : 0;
+  const bool active = qg < QG;
+  const int o0 = O <= (int)blockDim.x ? (int)threadIdx.x % O : (int)threadIdx.x;
+  const int ostep = O <= (int)blockDim.x ? O : (int)blockDim.x;
+  const int64_t nW = (int64_t)O * Dr * B;
+  for (int64_t e = threadIdx.x; e < QG * nW; e += blockDim.x) acc[e] = 0.f;
+  float* accq = acc + (active ? qg : 0) * nW;
   const int64_t lo = (P * blockIdx.x) / gridDim.x, hi = (P * (blockIdx.x + 1)) / gridDim.x;
   float dbs[2] = {0.f, 0.f};              // O <= 2 * FL_THREADS
   for (int64_t p0 = lo; p0 < hi; p0 += FL_BATCH) {
@@ -163,15 +178,23 @@ __global__ void __launch_bounds__(FL_THREADS) k_wgrad_first(const float* __restr
       }
     }
     __syncthreads();
+    if (!active) continue;
     const int nq = (int)(pe - p0);
-    for (int oo = 0; oo < 2; ++oo) {
-      const int o = threadIdx.x + oo * blockDim.x;
-      if (o >= O) break;
-      for (int q = 0; q < nq; ++q) {
-        const float* yb = Ybar + (p0 + q) * (int64_t)(C * O) + o;
+    int oo = 0;
+    for (int o = o0; o < O; o += ostep, ++oo) {
+      // the next point's adjoint row is loaded while this one is accumulated (latency hiding)
+      float yn[C];
+#pragma unroll
+      for (int c = 0; c < C; ++c) yn[c] = (qg < nq) ? __ldg(Ybar + (p0 + qg) * (int64_t)(C * O) + c * O + o) : 0.f;
+      for (int q = qg; q < nq; q += QG) {
         float y[C];
 #pragma unroll
-        for (int c = 0; c < C; ++c) y[c] = __ldg(yb + c * O);
+        for (int c = 0; c < C; ++c) y[c] = yn[c];
+        if (q + QG < nq) {
+          const float* ybn = Ybar + (p0 + q + QG) * (int64_t)(C * O) + o;
+#pragma unroll
+          for (int c = 0; c < C; ++c) yn[c] = __ldg(ybn + c * O);
+        }
         dbs[oo] += y[0];
         for (int a = 0; a < Dr; ++a) {
           const FlBasis& t = tab[q * Dr + a];
@@ -187,21 +210,30 @@ __global__ void __launch_bounds__(FL_THREADS) k_wgrad_first(const float* __restr
             if (r > bc.k) break;
             const int n = t.n0 + r;
             if (n < 0 || n >= B) continue;
-            acc[(a * B + n) * O + o] += fmaf(y[0], t.v[0][r], fmaf(y1, t.v[1][r], y2 * t.v[2][r]));
+            accq[(a * B + n) * O + o] += fmaf(y[0], t.v[0][r], fmaf(y1, t.v[1][r], y2 * t.v[2][r]));
           }
         }
       }
     }
   }
+  // fixed-order sum over the point groups
+  dbs_sh[threadIdx.x] = active ? dbs[0] : 0.f;
+  dbs_sh[FL_THREADS + threadIdx.x] = active ? dbs[1] : 0.f;
   __syncthreads();
-  const int64_t nW = (int64_t)O * Dr * B;
-  for (int oo = 0; oo < 2; ++oo) {
-    const int o = threadIdx.x + oo * blockDim.x;
-    if (o >= O) break;
-    float* dst = part + blockIdx.x * nW + (int64_t)o * Dr * B;
-    for (int a = 0; a < Dr; ++a)
-      for (int n = 0; n < B; ++n) dst[a * B + n] = acc[(a * B + n) * O + o];
-    part_b[blockIdx.x * (int64_t)O + o] = dbs[oo];
+  for (int64_t e = threadIdx.x; e < nW; e += blockDim.x) {
+    float v = 0.f;
+    for (int g = 0; g < QG; ++g) v += acc[g * nW + e];
+    const int o = (int)(e % O), an = (int)(e / O);          // acc index (a*B + n)*O + o
+    part[blockIdx.x * nW + (int64_t)o * Dr * B + an] = v;
+  }
+  for (int o = threadIdx.x; o < O; o += blockDim.x) {
+    float v = 0.f;
+    if (O <= (int)blockDim.x) {
+      for (int g = 0; g < QG; ++g) v += dbs_sh[g * O + o];
+    } else {
+      v = dbs_sh[(o / blockDim.x) * FL_THREADS + (o % blockDim.x)];
+    }
+    part_b[blockIdx.x * (int64_t)O + o] = v;
   }
 }
 

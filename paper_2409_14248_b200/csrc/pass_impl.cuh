@@ -117,7 +117,7 @@ hrkan_status run_pass(hrkan_net* net, const PassArgs& a, cudaStream_t st) {
         const unsigned grid = (unsigned)((tot + 255) / 256);
         const int cls = (l == 0) ? HRKAN_K_FWD_FIRST : HRKAN_K_FWD_HIDDEN;
         if (l == 0) {
-          const int bd = std::min(FL_THREADS, (O + 31) / 32 * 32);
+          const int bd = FL_THREADS;
           const unsigned gf = (unsigned)std::min<int64_t>((n + FL_BATCH - 1) / FL_BATCH, 16 * net->num_sms);
           HR_LAUNCH(cls, "k_fwd_first", k_fwd_first<NF, NS, M><<<gf, bd, 0, st>>>(in, net->wt[l], net->params + net->b_off[l], jet[l + 1], n, I, O, bc));
         } else
@@ -173,10 +173,11 @@ hrkan_status run_pass(hrkan_net* net, const PassArgs& a, cudaStream_t st) {
         if (l == 0) {
           // first layer: batched shared basis tables, one thread per output neuron
           auto kfn = k_wgrad_first<NF, NS, M>;
-          const size_t fsm = sizeof(float) * (size_t)I * net->B * O;
+          const int QG = O <= FL_THREADS ? FL_THREADS / O : 1;
+          const size_t fsm = sizeof(float) * (size_t)QG * I * net->B * O;
           if (fsm > 200 * 1024 || O > 2 * FL_THREADS) return fail(HRKAN_EUNSUPPORTED, "first layer too wide");
           if (fsm > 48 * 1024) HR_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm));
-          const int bd = std::min(FL_THREADS, (O + 31) / 32 * 32);
+          const int bd = FL_THREADS;
           const int nzf = (int)std::max<int64_t>(1, std::min<int64_t>(2 * net->num_sms, n / 64));
           const int64_t nWf = (int64_t)O * I * net->B;
           HR_CUDA(net->first_part.ensure(sizeof(float) * (size_t)nzf * (nWf + O)));

@@ -237,9 +237,14 @@ __global__ void k_reduce_parts(const float* __restrict__ part, const float* __re
                                int64_t nW, int O, float* __restrict__ dW, float* __restrict__ db) {
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t < nW) {
-    float s = 0.f;
-    for (int z = 0; z < nz; ++z) s += part[z * nW + t];
-    dW[t] += s;
+    float s0 = 0.f, s1 = 0.f;                      // 2 independent chains, combined in a fixed order
+    int z = 0;
+    for (; z + 2 <= nz; z += 2) {
+      s0 += part[z * nW + t];
+      s1 += part[(z + 1) * nW + t];
+    }
+    if (z < nz) s0 += part[z * nW + t];
+    dW[t] += s0 + s1;
   } else if (t < nW + O) {
     const int j = (int)(t - nW);
     float s = 0.f;
