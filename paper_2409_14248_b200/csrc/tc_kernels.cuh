@@ -473,7 +473,7 @@ hrkan_status launch_fwd_tc(hrkan_net* net, int l, const float* X, float* Y, int6
   const int cls = HRKAN_K_FWD_HIDDEN;
   HR_LAUNCH(cls, "k_fwd_tc",
             kfn<<<grid, TC_THREADS, Cfg::SMEM_BYTES, st>>>(tm, ls.w_fwd, net->params + net->b_off[l], Y, n, I, ls.nkb,
-                                                           Cfg::NACC == 2 ? net->tc_seg : 2 * net->tc_seg, net->bc,
+                                                           Cfg::NACC == 2 ? net->tc_seg : net->tc_seg_single, net->bc,
                                                            net->tc_dbg));
   return HRKAN_OK;
 }

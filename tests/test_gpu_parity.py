@@ -331,11 +331,12 @@ def test_init_distribution(torch_mod):
         assert abs(W.var() / var - 1) < 5 * math.sqrt(2.0 / n) + 1e-3
 
 
-def test_full_size_forward_sampled(torch_mod):
-    """Full BASELINE size (C3, 2^20 interior points, default chunking = bench launch config):
-    sampled outputs checked one by one against the oracle."""
+@pytest.mark.parametrize("key", ["C3", "C4", "C5"])
+def test_full_size_forward_sampled(torch_mod, key):
+    """Full BASELINE sizes (C3 2^20, C4 2^22, C5 2^24 interior points, default chunking = the bench
+    launch configuration): sampled outputs checked one by one against the oracle."""
     torch = torch_mod
-    w = HI.WORKLOADS["C3"]
+    w = HI.WORKLOADS[key]
     ps = HI.make_points(w)
     net, params = _make(w)
     u, du, d2u = [t.cpu().numpy() for t in net.forward_jet(torch.from_numpy(ps.interior).cuda())]
