@@ -253,161 +253,6 @@ __global__ void k_reduce_parts(const float* __restrict__ part, const float* __re
   }
 }
 
-// ---------------------------------------------------------------------------------------------
-// Last layer output -> residual, loss partial sums and backward seeds.
-//   Poisson: r = sum_a u_aa - f,  f = -D pi^2 prod_a sin(pi xi_a) (Eq. 3) or forcing[p];
-//            seeds dL/du_aa = g = 2 alpha r / N_int.
-//   Burgers: r = u_t + adv u u_x - visc u_xx (Eq. 5), jet channels (u, u_x, u_t, u_xx);
-//            seeds dL/du = g adv u_x, dL/du_x = g adv u, dL/du_t = g, dL/du_xx = -g visc.
-// Writes per-block partials of sum r^2 and of the non-finite count (deterministic block
-// reduction; the fixed-order grid reduction is k_finish_loss).
-// ---------------------------------------------------------------------------------------------
-template <int D, int NF, int NS, bool BURGERS>
-__global__ void __launch_bounds__(256) k_interior_loss(const float* __restrict__ Yl, const float* __restrict__ pts,
-                                                       const float* __restrict__ forcing, float* __restrict__ seeds,
-                                                       float* __restrict__ part, int64_t P, float alpha,
-                                                       float adv, float visc, float inv_n) {
-  constexpr int C = 1 + NF + NS;
-  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  float sq = 0.f, bad = 0.f;
-  if (p < P) {
-    float jet[C];
-#pragma unroll
-    for (int c = 0; c < C; ++c) jet[c] = Yl[p * C + c];
-    float r;
-    if (BURGERS) {
-      const float u = jet[0], ux = jet[1], ut = jet[2], uxx = jet[1 + NF];
-      r = ut + adv * u * ux - visc * uxx;
-    } else {
-      float f;
-      if (forcing) {
-        f = forcing[p];
-      } else {
-        float prod = 1.f;
-#pragma unroll
-        for (int a = 0; a < D; ++a) prod *= sinpif(pts[p * D + a]);
-        f = -(float)D * 9.8696044010893586f * prod;   // -D pi^2 prod sin(pi xi_a)
-      }
-      float lap = 0.f;
-#pragma unroll
-      for (int a = 0; a < NS; ++a) lap += jet[1 + NF + a];
-      r = lap - f;
-    }
-    sq = r * r;
-    bad = isfinite(r) ? 0.f : 1.f;
-    const float g = 2.f * alpha * r * inv_n;
-    float s[C];
-#pragma unroll
-    for (int c = 0; c < C; ++c) s[c] = 0.f;
-    if (BURGERS) {
-      s[0] = g * adv * jet[1];
-      s[1] = g * adv * jet[0];
-      s[2] = g;
-      s[1 + NF] = -g * visc;
-    } else {
-#pragma unroll
-      for (int a = 0; a < NS; ++a) s[1 + NF + a] = g;
-    }
-#pragma unroll
-    for (int c = 0; c < C; ++c) seeds[p * C + c] = s[c];
-  }
-  // block reduction (fixed order): warp shuffle then warp 0
-  __shared__ float red[2][32];
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    sq += __shfl_xor_sync(0xffffffffu, sq, o);
-    bad += __shfl_xor_sync(0xffffffffu, bad, o);
-  }
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  if (lane == 0) { red[0][wid] = sq; red[1][wid] = bad; }
-  __syncthreads();
-  if (wid == 0) {
-    const int nw = blockDim.x >> 5;
-    sq = lane < nw ? red[0][lane] : 0.f;
-    bad = lane < nw ? red[1][lane] : 0.f;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      sq += __shfl_xor_sync(0xffffffffu, sq, o);
-      bad += __shfl_xor_sync(0xffffffffu, bad, o);
-    }
-    if (lane == 0) { part[2 * blockIdx.x] = sq; part[2 * blockIdx.x + 1] = bad; }
-  }
-}
-
-// Boundary / initial value-only pass: e = u - g, seed dL/du = 2 e / N_bi.
-__global__ void __launch_bounds__(256) k_boundary_loss(const float* __restrict__ Yl, const float* __restrict__ g,
-                                                       float* __restrict__ seeds, float* __restrict__ part,
-                                                       int64_t P, float inv_n) {
-  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  float sq = 0.f, bad = 0.f;
-  if (p < P) {
-    const float e = Yl[p] - g[p];
-    sq = e * e;
-    bad = isfinite(e) ? 0.f : 1.f;
-    seeds[p] = 2.f * e * inv_n;
-  }
-  __shared__ float red[2][32];
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    sq += __shfl_xor_sync(0xffffffffu, sq, o);
-    bad += __shfl_xor_sync(0xffffffffu, bad, o);
-  }
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  if (lane == 0) { red[0][wid] = sq; red[1][wid] = bad; }
-  __syncthreads();
-  if (wid == 0) {
-    const int nw = blockDim.x >> 5;
-    sq = lane < nw ? red[0][lane] : 0.f;
-    bad = lane < nw ? red[1][lane] : 0.f;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      sq += __shfl_xor_sync(0xffffffffu, sq, o);
-      bad += __shfl_xor_sync(0xffffffffu, bad, o);
-    }
-    if (lane == 0) { part[2 * blockIdx.x] = sq; part[2 * blockIdx.x + 1] = bad; }
-  }
-}
-
-// out_loss += scale * sum_b part[2b] (double accumulation, fixed order); out_flag += sum part[2b+1].
-__global__ void k_finish_loss(const float* __restrict__ part, int nb, float scale, float* __restrict__ out_loss,
-                              float* __restrict__ out_flag) {
-  __shared__ double red[2][32];
-  double sq = 0.0, bad = 0.0;
-  for (int b = threadIdx.x; b < nb; b += blockDim.x) {
-    sq += (double)part[2 * b];
-    bad += (double)part[2 * b + 1];
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    sq += __shfl_xor_sync(0xffffffffu, sq, o);
-    bad += __shfl_xor_sync(0xffffffffu, bad, o);
-  }
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  if (lane == 0) { red[0][wid] = sq; red[1][wid] = bad; }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double s = 0.0, f = 0.0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { s += red[0][w]; f += red[1][w]; }
-    *out_loss += (float)(s * (double)scale);
-    *out_flag += (float)f;
-  }
-}
-
-// Scatter the last layer's jet [P][C] (O = 1) into u[P], du[P][D], d2u[P][D].
-template <int D>
-__global__ void k_scatter_jet(const float* __restrict__ Yl, int64_t P, float* __restrict__ u, float* __restrict__ du,
-                              float* __restrict__ d2u) {
-  constexpr int C = 1 + 2 * D;
-  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (p >= P) return;
-  if (u) u[p] = Yl[p * C];
-#pragma unroll
-  for (int a = 0; a < D; ++a) {
-    if (du) du[p * D + a] = Yl[p * C + 1 + a];
-    if (d2u) d2u[p * D + a] = Yl[p * C + 1 + D + a];
-  }
-}
-
 // W[j][i][n] -> Wt[i][n][j]
 __global__ void k_transpose_w(const float* __restrict__ W, float* __restrict__ Wt, int O, int IB) {
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
