@@ -156,7 +156,6 @@ hrkan_status hrkan_create(const int32_t* widths, int32_t n_widths, int32_t G, in
   if (const char* e = std::getenv("HRKAN_TC_SEG")) net->tc_seg = net->tc_seg_single = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("HRKAN_TC_WSEG")) net->tc_wseg = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("HRKAN_TC_DBG")) net->tc_dbg = std::atoi(e);
-  if (const char* e = std::getenv("HRKAN_TC_DPAIR")) net->tc_dpair = std::atoi(e);
   auto cleanup = [&](hrkan_status s) {
     hrkan_free(net);
     return s;

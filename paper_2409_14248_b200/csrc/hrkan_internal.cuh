@@ -135,7 +135,6 @@ struct hrkan_net {
   int tc_seg_single = 160;              // ... single accumulator (the drain stalls the MMA): C5 -> 2 segments
   int tc_wseg = 256;                    // wgrad stages per TMEM drain into the fp32 master
   int tc_dbg = 0;                       // timing-experiment switches (HRKAN_TC_DBG; 0 in production)
-  int tc_dpair = 1;                     // dgrad: CTA pairs share multicast Ybar stages (HRKAN_TC_DPAIR=0: off)
   // CUDA-graph replay of hrkan_pinn_loss_grad (hrkan_set_graph_mode)
   bool graph_mode = false;
   GraphKey graph_key{};

@@ -69,14 +69,10 @@ __global__ void k_tile_w_dgr(const float* __restrict__ W, uint16_t* __restrict__
   dst[per + r8] = lo;
 }
 
-// PAIR: a cluster of two CTAs takes one point tile and splits its M-tiles (mt = 2j + rank); the
-// pre-split Ybar stage, identical for both, is fetched from L2 once and multicast into both CTAs (each
-// CTA issues one half), which halves the kernel's L2 -> SM stream (it is bound by it otherwise).  A
-// stage slot is refilled only after BOTH CTAs' MMAs released it (multicast commits, count 2).
-template <int NF, int NS, int M, int OO, bool PAIR>
+template <int NF, int NS, int M, int OO>
 __global__ void __launch_bounds__(DGR_THREADS, 1)
     k_dgrad_tc(const __grid_constant__ CUtensorMap tmX, const uint16_t* __restrict__ Ysplit,
-               const uint16_t* __restrict__ Wtiled, float* __restrict__ Xbar, int64_t P, int I, int IPT, int nmt_all,
+               const uint16_t* __restrict__ Wtiled, float* __restrict__ Xbar, int64_t P, int I, int IPT, int nmt,
                BasisCfg bc, int dbg) {
   using Cfg = DgrCfg<NF, NS, M, OO>;
   constexpr int C = Cfg::C, NP = Cfg::NP, N = Cfg::N, NKB = Cfg::NKB, NSTAGE = Cfg::NSTAGE;
@@ -90,17 +86,13 @@ __global__ void __launch_bounds__(DGR_THREADS, 1)
   __shared__ __align__(8) uint64_t jet_full[2], jet_empty[2];
   __shared__ uint32_t tmem_base_sh;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int rank = PAIR ? (int)tc::cluster_ctarank() : 0;
-  const int64_t tile = PAIR ? (int64_t)(blockIdx.x >> 1) : (int64_t)blockIdx.x;
-  const int64_t p0 = tile * NP;
-  const int nmt = PAIR ? (nmt_all + 1) / 2 : nmt_all;   // this CTA's M-tiles: global mt = MT(j)
-  auto MT = [&](int j) { return PAIR ? 2 * j + rank : j; };
+  const int64_t p0 = (int64_t)blockIdx.x * NP;
   const int nblk = nmt * NKB;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < NSTAGE; ++s) {
       tc::mbar_init(&full_bar[s], 1);
-      tc::mbar_init(&empty_bar[s], PAIR ? 2 : 1);
+      tc::mbar_init(&empty_bar[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       tc::mbar_init(&acc_full[a], 1);
@@ -112,8 +104,7 @@ __global__ void __launch_bounds__(DGR_THREADS, 1)
   }
   if (warp == DGR_MMA_WARP) tc::tmem_alloc<Cfg::TMEM_COLS>(&tmem_base_sh);
   tc::tc_fence_before();
-  if (PAIR) tc::cluster_sync();                   // peers' multicast copies / commits target our barriers
-  else __syncthreads();
+  __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem = tmem_base_sh;
 
@@ -123,14 +114,13 @@ __global__ void __launch_bounds__(DGR_THREADS, 1)
     const int half = warp >> 2;                   // which half of the slice columns this warp drains
     const int etid = threadIdx.x;
     const int r = qw * 32 + lane;                 // accumulator row = il*B + n
-    for (int j = 0; j < nmt; ++j) {
-      const int mt = MT(j);
-      const int buf = j & 1;
-      tc::mbar_wait(&acc_full[buf], (uint32_t)((j >> 1) & 1));
+    for (int mt = 0; mt < nmt; ++mt) {
+      const int buf = mt & 1;
+      tc::mbar_wait(&acc_full[buf], (uint32_t)((mt >> 1) & 1));
       tc::tc_fence_after();
-      tc::mbar_wait(&jet_full[buf], (uint32_t)((j >> 1) & 1));
+      tc::mbar_wait(&jet_full[buf], (uint32_t)((mt >> 1) & 1));
       const float* js = jets + buf * Cfg::JET_FLOATS + ((mt * IPT) & 3);   // [NP][C][IPTB] from input (mt*IPT) & ~3
-      const int n_in = max(0, min(IPT, I - mt * IPT));   // inputs in this tile (0: padding tile of a pair)
+      const int n_in = min(IPT, I - mt * IPT);    // inputs in this tile
 #pragma unroll 1
       for (int sl = 0; sl < NP / SLICE_P; ++sl) {
         const uint32_t tb = tmem + ((uint32_t)(qw * 32) << 16) + (uint32_t)(buf * N + sl * SLICE_P * C);
@@ -206,14 +196,14 @@ __global__ void __launch_bounds__(DGR_THREADS, 1)
   } else if (warp == DGR_MMA_WARP) {
     if (lane == 0) {
       constexpr uint32_t idesc = tc::idesc_bf16(128, N);
-      for (int jt = 0; jt < nmt; ++jt) {
-        const int buf = jt & 1;
-        if (jt >= 2) {
-          tc::mbar_wait(&acc_empty[buf], (uint32_t)(((jt >> 1) - 1) & 1));
+      for (int mt = 0; mt < nmt; ++mt) {
+        const int buf = mt & 1;
+        if (mt >= 2) {
+          tc::mbar_wait(&acc_empty[buf], (uint32_t)(((mt >> 1) - 1) & 1));
           tc::tc_fence_after();
         }
         for (int kb = 0; kb < NKB; ++kb) {
-          const int g = jt * NKB + kb, s = g % NSTAGE;
+          const int g = mt * NKB + kb, s = g % NSTAGE;
           tc::mbar_wait(&full_bar[s], (g / NSTAGE) & 1);
           tc::tc_fence_after();
           const uint32_t w_hi = tc::smem_u32(smem + s * Cfg::STAGE_BYTES);
@@ -228,8 +218,7 @@ __global__ void __launch_bounds__(DGR_THREADS, 1)
           tc::mma_bf16(d, wl, yh, idesc, kb > 0 ? 1u : 0u);
           tc::mma_bf16(d, wh, yl, idesc, 1u);
           tc::mma_bf16(d, wh, yh, idesc, 1u);
-          if (PAIR) tc::mma_commit_mc(&empty_bar[s], 3);   // the slot is shared with the peer's multicast
-          else tc::mma_commit(&empty_bar[s]);
+          tc::mma_commit(&empty_bar[s]);
         }
         tc::mma_commit(&acc_full[buf]);
       }
@@ -239,23 +228,16 @@ __global__ void __launch_bounds__(DGR_THREADS, 1)
     // ===================== producer: W^T and pre-split Ybar stages (1-D bulk copies); never waits on the
     // epilogue, so the MMA is only held back by the TMEM accumulators it releases early
     if (lane == 0) {
-      const uint16_t* ytile = Ysplit + tile * NKB * (Cfg::Y_STAGE_BYTES / 2);
+      const uint16_t* ytile = Ysplit + (int64_t)blockIdx.x * NKB * (Cfg::Y_STAGE_BYTES / 2);
       for (int g = 0; g < nblk; ++g) {
-        const int jt = g / NKB, kb = g - (g / NKB) * NKB;
-        const int mtw = min(MT(jt), nmt_all - 1);   // a pair's padding tile re-reads a valid W^T tile
+        const int kb = g - (g / NKB) * NKB;
         const int s = g % NSTAGE;
         tc::mbar_wait(&empty_bar[s], ((g / NSTAGE) & 1) ^ 1);
         tc::mbar_arrive_expect_tx(&full_bar[s], Cfg::STAGE_BYTES);
-        tc::bulk_g2s(smem + s * Cfg::STAGE_BYTES, Wtiled + ((int64_t)mtw * NKB + kb) * (Cfg::W_STAGE_BYTES / 2),
-                     Cfg::W_STAGE_BYTES, &full_bar[s]);
-        const uint16_t* ysrc = ytile + (int64_t)kb * (Cfg::Y_STAGE_BYTES / 2);
-        uint8_t* ydst = smem + s * Cfg::STAGE_BYTES + Cfg::W_STAGE_BYTES;
-        if (PAIR) {                                // each CTA multicasts one half (hi | lo) to both
-          tc::bulk_g2s_mc(ydst + rank * (Cfg::Y_STAGE_BYTES / 2), ysrc + rank * (Cfg::Y_STAGE_BYTES / 4),
-                          Cfg::Y_STAGE_BYTES / 2, &full_bar[s], 3);
-        } else {
-          tc::bulk_g2s(ydst, ysrc, Cfg::Y_STAGE_BYTES, &full_bar[s]);
-        }
+        tc::bulk_g2s(smem + s * Cfg::STAGE_BYTES, Wtiled + (int64_t)g * (Cfg::W_STAGE_BYTES / 2), Cfg::W_STAGE_BYTES,
+                     &full_bar[s]);
+        tc::bulk_g2s(smem + s * Cfg::STAGE_BYTES + Cfg::W_STAGE_BYTES, ytile + (int64_t)kb * (Cfg::Y_STAGE_BYTES / 2),
+                     Cfg::Y_STAGE_BYTES, &full_bar[s]);
       }
     }
     __syncwarp();
@@ -263,18 +245,17 @@ __global__ void __launch_bounds__(DGR_THREADS, 1)
     // ===================== jet producer: input-jet boxes of the M-tiles (TMA), two tiles ahead of use
     if (lane == 0) {
       tc::tma_prefetch_desc(&tmX);
-      for (int jt = 0; jt < nmt; ++jt) {
-        const int jb = jt & 1;
-        if (jt >= 2) tc::mbar_wait(&jet_empty[jb], (uint32_t)(((jt >> 1) - 1) & 1));
+      for (int mt = 0; mt < nmt; ++mt) {
+        const int jb = mt & 1;
+        if (mt >= 2) tc::mbar_wait(&jet_empty[jb], (uint32_t)(((mt >> 1) - 1) & 1));
         tc::mbar_arrive_expect_tx(&jet_full[jb], Cfg::JET_FLOATS * 4);
-        tc::tma_load_3d(jets + jb * Cfg::JET_FLOATS, &tmX, (MT(jt) * IPT) & ~3, 0, (int)p0, &jet_full[jb]);
+        tc::tma_load_3d(jets + jb * Cfg::JET_FLOATS, &tmX, (mt * IPT) & ~3, 0, (int)p0, &jet_full[jb]);
       }
     }
     __syncwarp();
   }
   tc::tc_fence_before();
-  if (PAIR) tc::cluster_sync();                   // no peer copy or commit may target an exited CTA
-  else __syncthreads();
+  __syncthreads();
   if (warp == DGR_MMA_WARP) tc::tmem_dealloc<Cfg::TMEM_COLS>(tmem);
 }
 

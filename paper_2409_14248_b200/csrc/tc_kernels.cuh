@@ -591,46 +591,20 @@ template <int NF, int NS, int M, int OO>
 hrkan_status launch_dgrad_tc(hrkan_net* net, int l, const float* X, const float* Ybar, float* Xbar, int64_t n,
                              cudaStream_t st) {
   using Cfg = DgrCfg<NF, NS, M, OO>;
+  auto kfn = k_dgrad_tc<NF, NS, M, OO>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    HR_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
+    attr_set = true;
+  }
   const TcLayerState& ls = net->tc_layers[l];
   const int I = net->widths[l];
   CUtensorMap tmX;
   HR_TRY(make_tmap_f32_3d(&tmX, X, (uint64_t)I, (uint64_t)Cfg::C, (uint64_t)n, DGR_IPTB, Cfg::C, Cfg::NP));
-  const unsigned ntile = (unsigned)((n + Cfg::NP - 1) / Cfg::NP);
-  const uint16_t* ysplit = (const uint16_t*)net->tc_yd.p;
-  if (net->tc_dpair) {
-    // cluster of two CTAs per point tile, Ybar stages multicast (tc_dgrad.cuh)
-    auto kfn = k_dgrad_tc<NF, NS, M, OO, true>;
-    static bool attr_set = false;
-    if (!attr_set) {
-      HR_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
-      attr_set = true;
-    }
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(2 * ntile);
-    cfg.blockDim = dim3(DGR_THREADS);
-    cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    HR_LAUNCH(HRKAN_K_DGRAD_HIDDEN, "k_dgrad_tc (pair)",
-              cudaLaunchKernelEx(&cfg, kfn, tmX, ysplit, (const uint16_t*)ls.w_dgr, Xbar, n, I, 128 / net->B,
-                                 ls.ntile_dgr, net->bc, net->tc_dbg));
-    return HRKAN_OK;
-  }
-  auto kfn = k_dgrad_tc<NF, NS, M, OO, false>;
-  static bool attr_set1 = false;
-  if (!attr_set1) {
-    HR_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
-    attr_set1 = true;
-  }
+  const unsigned grid = (unsigned)((n + Cfg::NP - 1) / Cfg::NP);
   HR_LAUNCH(HRKAN_K_DGRAD_HIDDEN, "k_dgrad_tc",
-            kfn<<<ntile, DGR_THREADS, Cfg::SMEM_BYTES, st>>>(tmX, ysplit, ls.w_dgr, Xbar, n, I, 128 / net->B,
-                                                             ls.ntile_dgr, net->bc, net->tc_dbg));
+            kfn<<<grid, DGR_THREADS, Cfg::SMEM_BYTES, st>>>(tmX, (const uint16_t*)net->tc_yd.p, ls.w_dgr, Xbar, n, I,
+                                                            128 / net->B, ls.ntile_dgr, net->bc, net->tc_dbg));
   return HRKAN_OK;
 }
 

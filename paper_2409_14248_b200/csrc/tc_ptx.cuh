@@ -239,25 +239,6 @@ __device__ __forceinline__ void mma_commit2(uint64_t* bar, uint16_t mask) {
       : "memory");
 }
 
-// cta_group::1 commit whose arrival goes to the same-offset mbarrier in every CTA of `mask`
-__device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask) {
-  asm volatile(
-      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
-          smem_u32(bar)),
-      "h"(mask)
-      : "memory");
-}
-// 1-D bulk copy global -> the same smem offset of every CTA in `mask`, complete_tx on each CTA's
-// same-offset mbarrier
-__device__ __forceinline__ void bulk_g2s_mc(void* dst_smem, const void* src_gmem, uint32_t bytes, uint64_t* bar,
-                                            uint16_t mask) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, [%3], %4;" ::
-          "r"(smem_u32(dst_smem)),
-      "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar)), "h"(mask)
-      : "memory");
-}
-
 // bf16x3 split: x = hi + lo + r with hi = bf16_rn(x), lo = bf16_rn(x - hi),
 // |r| <= 2^-18 |x|; a*b ~ ah*bh + ah*bl + al*bh (the dropped al*bl is <= 2^-18 |ab|).
 // Pairs are packed little-endian: the element at the lower K index sits in the low 16 bits.
