@@ -346,3 +346,23 @@ def test_full_size_forward_sampled(torch_mod, key):
     assert rel_l2(du[idx], odu) < TOL["du"]
     assert rel_l2(d2u[idx], od2u) < TOL["d2u"]
     assert np.all(np.isfinite(u)) and np.all(np.isfinite(d2u))
+
+
+def test_paper_poisson_training_converges(torch_mod):
+    """SURVEY §8(f) next row 1 (scripts/train_paper_poisson.py): the paper's Poisson experiment
+    ([2,2,1], g=5, k=3, m=4, alpha=0.05, 3000 Adam epochs on 960 + 120 points) trained entirely on
+    the B200 path lowers the loss by more than 10x and reaches a test MSE below 10 % of the grid
+    (the paper reports 0.0434 % mean with an unstated learning rate and init)."""
+    torch = torch_mod
+    import importlib.util
+    import os
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "scripts",
+                        "train_paper_poisson.py")
+    spec = importlib.util.spec_from_file_location("train_paper_poisson", path)
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    dev = torch.device("cuda:0")
+    r0 = mod.run(0, 1, 1e-2, dev)          # ~ the initial loss (one epoch)
+    r = mod.run(0, 3000, 1e-2, dev)
+    assert r["train_loss"] < 0.1 * r0["train_loss"]
+    assert r["test_mse_percent"] < 10.0
