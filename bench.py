@@ -87,9 +87,37 @@ def interior_channels(w: HI.Workload) -> int:
 # ------------------------------------------------------------------------------------------
 # clocks during the timed region (nvidia-smi sampler)
 # ------------------------------------------------------------------------------------------
+_NVML_POLLER = r"""
+import sys, threading, time, pynvml
+pynvml.nvmlInit()
+try:
+    h = pynvml.nvmlDeviceGetHandleByPciBusId(sys.argv[1])
+except Exception:
+    h = pynvml.nvmlDeviceGetHandleByIndex(int(sys.argv[2]))
+mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+stop, out = threading.Event(), []
+def poll():
+    while not stop.is_set():
+        out.append((pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM),
+                    pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)))
+        time.sleep(float(sys.argv[3]))
+t = threading.Thread(target=poll); t.start()
+print("ready", flush=True)
+sys.stdin.read()                      # runs until the parent closes stdin
+stop.set(); t.join()
+bits = {"hw_slowdown": pynvml.nvmlClocksEventReasonHwSlowdown,
+        "hw_thermal_slowdown": pynvml.nvmlClocksEventReasonHwThermalSlowdown,
+        "sw_thermal_slowdown": pynvml.nvmlClocksEventReasonSwThermalSlowdown,
+        "sw_power_cap": pynvml.nvmlClocksEventReasonSwPowerCap}
+for sm, r in out:
+    print(sm, mx, *[n for n, b in bits.items() if r & b])
+"""
+
+
 class ClockSampler:
-    """Samples the SM clock and the throttle reasons while the timed region runs: NVML polled every
-    millisecond from a thread (so even the sub-10 ms C1/C2 regions get samples), else nvidia-smi -lms."""
+    """Samples the SM clock and the throttle reasons while the timed region runs.  NVML is polled every
+    millisecond by a separate process that buffers its samples until the region ends (so it neither
+    competes for this interpreter's GIL nor misses the sub-10 ms C1/C2 regions); fallback nvidia-smi."""
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
@@ -98,62 +126,63 @@ class ClockSampler:
     def __init__(self, gpu_index: int):
         self.gpu = gpu_index
         self.proc = None
-        self.nvml = None
-        self.stop = threading.Event()
         self.sm, self.mx, self.reasons = [], None, set()
         self.source = "none"
 
-    def _nvml_handle(self):
-        import pynvml
-        import torch
-        pynvml.nvmlInit()
-        try:      # map the CUDA device to the NVML device by PCI bus id (CUDA_VISIBLE_DEVICES-proof)
+    def _bus_id(self):
+        try:
+            import torch
             pr = torch.cuda.get_device_properties(self.gpu)
-            bus = f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
-            h = pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+            return f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
         except Exception:
-            h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
-        bits = {"hw_slowdown": pynvml.nvmlClocksEventReasonHwSlowdown,
-                "hw_thermal_slowdown": pynvml.nvmlClocksEventReasonHwThermalSlowdown,
-                "sw_thermal_slowdown": pynvml.nvmlClocksEventReasonSwThermalSlowdown,
-                "sw_power_cap": pynvml.nvmlClocksEventReasonSwPowerCap}
-        return pynvml, h, bits
+            return "none"
 
     def __enter__(self):
-        try:
-            self.nvml = self._nvml_handle()
-            pynvml, h, _ = self.nvml
-            self.mx = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
-            self.source = "nvml"
-            self.t = threading.Thread(target=self._poll_nvml, daemon=True)
-            self.t.start()
+        if os.environ.get("BENCH_CLOCK_PERIOD_S") == "off":
             return self
+        try:
+            self.proc = subprocess.Popen([sys.executable, "-c", _NVML_POLLER, self._bus_id(), str(self.gpu),
+                                          os.environ.get("BENCH_CLOCK_PERIOD_S", "0.001")],
+                                         stdin=subprocess.PIPE, stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            if self.proc.stdout.readline().strip() == "ready":
+                self.source = "nvml"
+                return self
+            self.proc.kill()
         except Exception:
-            self.nvml = None
+            pass
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
                                           "--format=csv,noheader,nounits", "-lms", "200"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.source = "nvidia-smi"
-            self.t = threading.Thread(target=self._read_smi, daemon=True)
-            self.t.start()
         except Exception:
             self.proc = None
         return self
 
-    def _poll_nvml(self):
-        pynvml, h, bits = self.nvml
-        while not self.stop.is_set():
+    def __exit__(self, *a):
+        if not self.proc:
+            return
+        if self.source == "nvml":
             try:
-                self.sm.append(float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)))
-                r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
-                self.reasons.update(n for n, b in bits.items() if r & b)
+                text, _ = self.proc.communicate(input="", timeout=30)
             except Exception:
+                self.proc.kill()
                 return
-            time.sleep(0.001)
-
-    def _read_smi(self):
-        for line in self.proc.stdout:
+            for line in text.splitlines():
+                parts = line.split()
+                if len(parts) >= 2:
+                    self.sm.append(float(parts[0]))
+                    self.mx = float(parts[1])
+                    self.reasons.update(parts[2:])
+            return
+        self.proc.terminate()
+        try:
+            text, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            return
+        for line in text.splitlines():
             parts = [p.strip() for p in line.strip().split(",")]
             if len(parts) < 7:
                 continue
@@ -165,17 +194,6 @@ class ClockSampler:
             for n, v in zip(self.NAMES, parts[3:7]):
                 if v.lower().startswith("active"):
                     self.reasons.add(n)
-
-    def __exit__(self, *a):
-        self.stop.set()
-        if self.nvml:
-            self.t.join(timeout=5)
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:
-                self.proc.kill()
 
     def summary(self):
         if not self.sm:
