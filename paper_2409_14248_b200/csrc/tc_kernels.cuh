@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   constexpr int NMT = Cfg::NMT, OP = Cfg::OP;
   constexpr int ACSB = Cfg::ACSB;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);   // keeps the shared address space visible to the compiler (STS/LDS, not generic ST/LD)
   float* win = reinterpret_cast<float*>(smem + NSTAGE * Cfg::STAGE_BYTES);   // [TC_NWIN][NP][C][TC_WIN]
   float* ctr = win + TC_NWIN * Cfg::WIN_FLOATS;              // basis centres mid_n, n < B
   __shared__ __align__(8) uint64_t full_bar[NSTAGE], empty_bar[NSTAGE], acc_full[NACC], acc_empty[NACC];
