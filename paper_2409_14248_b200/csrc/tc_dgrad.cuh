@@ -43,7 +43,10 @@ struct DgrCfg {
   static_assert(NSTAGE >= 3, "shared memory budget");
   static_assert(STAGE_BYTES % 128 == 0, "TMA boxes after the stages need 128-B alignment");
 };
-constexpr int DGR_EPI_WARPS = 8;       // two epilogue warps per TMEM lane quadrant
+#ifndef HRKAN_DGR_EPI_WARPS
+#define HRKAN_DGR_EPI_WARPS 8
+#endif
+constexpr int DGR_EPI_WARPS = HRKAN_DGR_EPI_WARPS;       // two epilogue warps per TMEM lane quadrant
 constexpr int DGR_THREADS = 32 * (DGR_EPI_WARPS + 3);   // + MMA warp + stage producer + jet producer
 constexpr int DGR_MMA_WARP = DGR_EPI_WARPS, DGR_PROD_WARP = DGR_EPI_WARPS + 1, DGR_JET_WARP = DGR_EPI_WARPS + 2;
 

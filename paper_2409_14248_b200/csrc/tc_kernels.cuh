@@ -28,7 +28,10 @@ using namespace hrkan;
 
 constexpr int TC_KB = 16;          // K per pipeline stage (two tf32 MMA K-steps of 8)
 constexpr int TC_GEN_THREADS = 128;   // one generator group (4 warps); the group handles every other K-block
-constexpr int TC_NGEN = 3;            // generator groups (all also drain the accumulators)
+#ifndef HRKAN_FWD_NGEN
+#define HRKAN_FWD_NGEN 3
+#endif
+constexpr int TC_NGEN = HRKAN_FWD_NGEN;            // generator groups (all also drain the accumulators)
 constexpr int TC_MMA_WARP = 4 * TC_NGEN, TC_PROD_WARP = 4 * TC_NGEN + 1, TC_WIN_WARP = 4 * TC_NGEN + 2;
 constexpr int TC_THREADS = 32 * (4 * TC_NGEN + 3);   // + MMA warp + W producer warp + jet-window TMA warp
 constexpr int TC_WIN = 4;             // inputs per jet window (16-B TMA rows)

@@ -29,7 +29,13 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
                "r"(bytes)
                : "memory");
 }
+// try_wait suspends the waiting warp until the phase completes or this many ns pass (instead of the
+// short default window), so waiting warps stop stealing issue slots from the generator warps.
+#ifndef MBAR_SUSPEND_NS
+#define MBAR_SUSPEND_NS 0
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#if MBAR_SUSPEND_NS == 0
   asm volatile(
       "{\n\t.reg .pred p;\n"
       "WAIT_%=:\n\t"
@@ -37,6 +43,15 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
+#else
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity), "r"(MBAR_SUSPEND_NS)
+      : "memory");
+#endif
 }
 
 // generic-proxy smem writes -> visible to the async proxy (tensor core / bulk copy)

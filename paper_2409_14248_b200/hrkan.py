@@ -15,6 +15,8 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "_lib", "libhrkan.so")
+if os.environ.get("HRKAN_LIB"):             # experiment variants only (scripts/build_variant.py)
+    LIB_PATH = os.environ["HRKAN_LIB"]
 
 HRKAN_POISSON = 0
 HRKAN_BURGERS = 1
