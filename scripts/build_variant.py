@@ -11,4 +11,6 @@ name, defines = sys.argv[1], tuple(sys.argv[2:])
 out = os.path.join(g.PKG, "_lib", "variants", name, "libhrkan.so")
 os.makedirs(os.path.dirname(out), exist_ok=True)
 g.build(force=True, defines=defines, so=out, load=False)
+import shutil  # noqa: E402
+shutil.rmtree(os.path.join(os.path.dirname(out), "obj"), ignore_errors=True)   # keep gpurun snapshots small
 print(out)
