@@ -28,12 +28,15 @@ using namespace hrkan;
 
 constexpr int TC_KB = 16;          // K per pipeline stage (two tf32 MMA K-steps of 8)
 constexpr int TC_GEN_THREADS = 128;   // one generator group (4 warps); the group handles every other K-block
+// Generator groups (all also drain the accumulators): 4 where the register budget of 19 warps allows
+// it without spills (measured: C4 forward 4.24 -> 3.78 ms, C3 1.83 -> 1.68 ms per 2^18 points), else 3
+// (C = 3 and C = 5 at O >= 128 spill with 4; C5's C = 7 layer was 2 % slower with 4).
 #ifndef HRKAN_FWD_NGEN
-#define HRKAN_FWD_NGEN 3
+#define HRKAN_FWD_NGEN 0
 #endif
-constexpr int TC_NGEN = HRKAN_FWD_NGEN;            // generator groups (all also drain the accumulators)
-constexpr int TC_MMA_WARP = 4 * TC_NGEN, TC_PROD_WARP = 4 * TC_NGEN + 1, TC_WIN_WARP = 4 * TC_NGEN + 2;
-constexpr int TC_THREADS = 32 * (4 * TC_NGEN + 3);   // + MMA warp + W producer warp + jet-window TMA warp
+__host__ __device__ constexpr int tc_ngen(int C, int O) {
+  return HRKAN_FWD_NGEN > 0 ? HRKAN_FWD_NGEN : (C == 1 || C == 4 || O <= 64) ? 4 : 3;
+}
 constexpr int TC_WIN = 4;             // inputs per jet window (16-B TMA rows)
 constexpr int TC_NWIN = 8;            // jet-window ring depth
 
@@ -68,11 +71,17 @@ struct FwdCfg {
   static constexpr int NSTAGE = NSTAGE_FIT > 6 ? 6 : NSTAGE_FIT;
   static constexpr int SMEM_BYTES = NSTAGE * STAGE_BYTES + FIXED_BYTES;
   static constexpr int NACC = (2 * NMT * N <= 512) ? 2 : 1;   // double-buffered accumulators if they fit
+  static constexpr int NGEN = tc_ngen(C, OO);
+  static constexpr int MMA_WARP = 4 * NGEN, PROD_WARP = 4 * NGEN + 1, WIN_WARP = 4 * NGEN + 2;
+  static constexpr int THREADS = 32 * (4 * NGEN + 3);        // + MMA warp + W producer warp + jet-window TMA warp
   static constexpr uint32_t TMEM_COLS = tc_tmem_cols(NACC * NMT * N);
   static_assert(N % 16 == 0 && N <= 256, "bad N");
   static_assert(NMT * N <= 512, "accumulators exceed TMEM");
   static_assert(NSTAGE >= 2, "shared memory budget");
   static_assert(STAGE_BYTES % 128 == 0, "TMA windows after the stages need 128-B alignment");
+  // groups write alternate K-blocks: a group's previous stage is NGEN back, so its lead over the oldest
+  // unconsumed stage stays below two laps of the ring (no parity aliasing on empty_bar) iff NGEN <= NSTAGE
+  static_assert(NGEN <= NSTAGE, "stage ring shallower than the generator groups");
 };
 
 // Pre-tiled, pre-split weights for k_fwd_tc: for K-block kb: [hi | lo] each [2 chunks][OP][8] bf16
@@ -100,13 +109,14 @@ __global__ void k_tile_w_fwd(const float* __restrict__ W, uint16_t* __restrict__
 //   warp 10      TMA loads of jet windows: X[p0 .. p0+NP)[C][8w .. 8w+8) -> smem ring (TC_NWIN deep),
 //                so the generators read the jets from shared memory (coalesced, latency hidden).
 template <int NF, int NS, int M, int OO>
-__global__ void __launch_bounds__(TC_THREADS, 1)
+__global__ void __launch_bounds__(FwdCfg<NF, NS, M, OO>::THREADS, 1)
     k_fwd_tc(const __grid_constant__ CUtensorMap tmX, const uint16_t* __restrict__ Wtiled, const float* __restrict__ bias,
              float* __restrict__ Y, int64_t P, int I, int nkb, int seg, BasisCfg bc, int dbg) {
   using Cfg = FwdCfg<NF, NS, M, OO>;
   constexpr int C = Cfg::C, NP = Cfg::NP, N = Cfg::N, O = Cfg::O, NACC = Cfg::NACC, NSTAGE = Cfg::NSTAGE;
   constexpr int NMT = Cfg::NMT, OP = Cfg::OP;
   constexpr int ACSB = Cfg::ACSB;
+  constexpr int TC_NGEN = Cfg::NGEN, TC_MMA_WARP = Cfg::MMA_WARP, TC_PROD_WARP = Cfg::PROD_WARP;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);   // keeps the shared address space visible to the compiler (STS/LDS, not generic ST/LD)
   float* win = reinterpret_cast<float*>(smem + NSTAGE * Cfg::STAGE_BYTES);   // [TC_NWIN][NP][C][TC_WIN]
@@ -475,7 +485,7 @@ hrkan_status launch_fwd_tc(hrkan_net* net, int l, const float* X, float* Y, int6
   const unsigned grid = (unsigned)((n + Cfg::NP - 1) / Cfg::NP);
   const int cls = HRKAN_K_FWD_HIDDEN;
   HR_LAUNCH(cls, "k_fwd_tc",
-            kfn<<<grid, TC_THREADS, Cfg::SMEM_BYTES, st>>>(tm, ls.w_fwd, net->params + net->b_off[l], Y, n, I, ls.nkb,
+            kfn<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, st>>>(tm, ls.w_fwd, net->params + net->b_off[l], Y, n, I, ls.nkb,
                                                            Cfg::NACC == 2 ? net->tc_seg : net->tc_seg_single, net->bc,
                                                            net->tc_dbg));
   return HRKAN_OK;
