@@ -16,7 +16,26 @@
 
 namespace {
 
-__host__ __device__ constexpr int dgr_slice_p(int C) { return C == 1 ? 64 : 16; }
+// Epilogue parallelism: a slice of SLICE_P points gives SLICE_P * IPT (point, input) gather tasks per
+// barrier interval; slices and epilogue warps are sized so those tasks fill the epilogue threads
+// (measured per 2^18 points: C4's C = 4 layers with 32-point slices and 12 warps 3.58 -> 2.65 ms, C3's
+// C = 5 layers with 24-point slices 1.29 -> 1.08 ms; C5's 7-channel slices stay at 16 points, 32 would
+// leave room for only 3 stages and was 30 % slower).
+#ifndef HRKAN_DGR_SLICE_P
+#define HRKAN_DGR_SLICE_P 0
+#endif
+#ifndef HRKAN_DGR_EPI_WARPS
+#define HRKAN_DGR_EPI_WARPS 0
+#endif
+__host__ __device__ constexpr int dgr_slice_p(int C) {
+  return (HRKAN_DGR_SLICE_P > 0 && C > 1 && tc_np(C) % (HRKAN_DGR_SLICE_P > 0 ? HRKAN_DGR_SLICE_P : 1) == 0 &&
+          (HRKAN_DGR_SLICE_P * C) % 8 == 0)
+             ? HRKAN_DGR_SLICE_P
+             : C == 1 ? 64 : C == 4 ? 32 : C == 5 ? 24 : 16;
+}
+__host__ __device__ constexpr int dgr_epi_warps(int C) {
+  return HRKAN_DGR_EPI_WARPS > 0 ? HRKAN_DGR_EPI_WARPS : C == 4 ? 12 : 8;
+}
 constexpr int DGR_SST = 129;   // column stride of the epilogue slice (odd: conflict-free gathers)
 constexpr int DGR_IPTB = 16;   // jet box width (inputs) >= IPT + 3 (box start aligned down to 16 B), B >= 11
 
@@ -38,17 +57,14 @@ struct DgrCfg {
   static constexpr int NSTAGE = NSTAGE_FIT > 8 ? 8 : NSTAGE_FIT;
   static constexpr int SMEM_BYTES = NSTAGE * STAGE_BYTES + FIXED_BYTES;
   static constexpr uint32_t TMEM_COLS = tc_tmem_cols(2 * N);
+  static constexpr int EPI_WARPS = dgr_epi_warps(C);           // multiple of 4 (TMEM lane quadrants)
+  static constexpr int THREADS = 32 * (EPI_WARPS + 3);          // + MMA warp + stage producer + jet producer
+  static constexpr int MMA_WARP = EPI_WARPS, PROD_WARP = EPI_WARPS + 1, JET_WARP = EPI_WARPS + 2;
   static_assert(N % 16 == 0 && N <= 256, "bad N");
-  static_assert(NP % SLICE_P == 0 && (SLICE_P * C) % 16 == 0, "bad slice");
+  static_assert(NP % SLICE_P == 0 && (SLICE_P * C) % 8 == 0 && EPI_WARPS % 4 == 0, "bad slice");
   static_assert(NSTAGE >= 3, "shared memory budget");
   static_assert(STAGE_BYTES % 128 == 0, "TMA boxes after the stages need 128-B alignment");
 };
-#ifndef HRKAN_DGR_EPI_WARPS
-#define HRKAN_DGR_EPI_WARPS 8
-#endif
-constexpr int DGR_EPI_WARPS = HRKAN_DGR_EPI_WARPS;       // two epilogue warps per TMEM lane quadrant
-constexpr int DGR_THREADS = 32 * (DGR_EPI_WARPS + 3);   // + MMA warp + stage producer + jet producer
-constexpr int DGR_MMA_WARP = DGR_EPI_WARPS, DGR_PROD_WARP = DGR_EPI_WARPS + 1, DGR_JET_WARP = DGR_EPI_WARPS + 2;
 
 // W^T tiles for k_dgrad_tc: for M-tile mt (inputs mt*IPT ...), K-block kb (o = kb*KB ...):
 // [hi | lo] each [2 chunks][128 rows][8] bf16, row = il*B + n (il < IPT), zero outside.
@@ -73,14 +89,16 @@ __global__ void k_tile_w_dgr(const float* __restrict__ W, uint16_t* __restrict__
 }
 
 template <int NF, int NS, int M, int OO>
-__global__ void __launch_bounds__(DGR_THREADS, 1)
+__global__ void __launch_bounds__(DgrCfg<NF, NS, M, OO>::THREADS, 1)
     k_dgrad_tc(const __grid_constant__ CUtensorMap tmX, const uint16_t* __restrict__ Ysplit,
                const uint16_t* __restrict__ Wtiled, float* __restrict__ Xbar, int64_t P, int I, int IPT, int nmt,
                BasisCfg bc, int dbg) {
   using Cfg = DgrCfg<NF, NS, M, OO>;
   constexpr int C = Cfg::C, NP = Cfg::NP, N = Cfg::N, NKB = Cfg::NKB, NSTAGE = Cfg::NSTAGE;
   constexpr int SLICE_P = Cfg::SLICE_P;
+  constexpr int DGR_EPI_WARPS = Cfg::EPI_WARPS, DGR_MMA_WARP = Cfg::MMA_WARP, DGR_PROD_WARP = Cfg::PROD_WARP;
   constexpr int NEPI = 32 * DGR_EPI_WARPS;
+  constexpr int NH = DGR_EPI_WARPS / 4;                       // epilogue warps per TMEM lane quadrant
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);   // keeps the shared address space visible to the compiler (STS/LDS, not generic ST/LD)
   float* jets = reinterpret_cast<float*>(smem + NSTAGE * Cfg::STAGE_BYTES);   // [2][NP][C][IPTB] input jets
@@ -114,7 +132,7 @@ __global__ void __launch_bounds__(DGR_THREADS, 1)
   if (warp < DGR_EPI_WARPS) {
     // ===================== epilogue: per M-tile, TMEM -> smem slices -> jet-chain gather
     const int qw = warp & 3;                      // TMEM lane quadrant (warp % 4)
-    const int half = warp >> 2;                   // which half of the slice columns this warp drains
+    const int half = warp >> 2;                   // which of the NH column phases this warp drains
     const int etid = threadIdx.x;
     const int r = qw * 32 + lane;                 // accumulator row = il*B + n
     for (int mt = 0; mt < nmt; ++mt) {
@@ -128,7 +146,7 @@ __global__ void __launch_bounds__(DGR_THREADS, 1)
       for (int sl = 0; sl < NP / SLICE_P; ++sl) {
         const uint32_t tb = tmem + ((uint32_t)(qw * 32) << 16) + (uint32_t)(buf * N + sl * SLICE_P * C);
 #pragma unroll 1
-        for (int c8 = half * 8; c8 < SLICE_P * C; c8 += 16) {
+        for (int c8 = half * 8; c8 < SLICE_P * C; c8 += 8 * NH) {
           float v[8];
           tc::tmem_ld8(tb + c8, v);
 #pragma unroll

@@ -616,7 +616,7 @@ hrkan_status launch_dgrad_tc(hrkan_net* net, int l, const float* X, const float*
   HR_TRY(make_tmap_f32_3d(&tmX, X, (uint64_t)I, (uint64_t)Cfg::C, (uint64_t)n, DGR_IPTB, Cfg::C, Cfg::NP));
   const unsigned grid = (unsigned)((n + Cfg::NP - 1) / Cfg::NP);
   HR_LAUNCH(HRKAN_K_DGRAD_HIDDEN, "k_dgrad_tc",
-            kfn<<<grid, DGR_THREADS, Cfg::SMEM_BYTES, st>>>(tmX, (const uint16_t*)net->tc_yd.p, ls.w_dgr, Xbar, n, I,
+            kfn<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, st>>>(tmX, (const uint16_t*)net->tc_yd.p, ls.w_dgr, Xbar, n, I,
                                                             128 / net->B, ls.ntile_dgr, net->bc, net->tc_dbg));
   return HRKAN_OK;
 }
