@@ -382,7 +382,7 @@ namespace {
 template <int C, int O>
 __global__ void __launch_bounds__(256) k_split_ybar(const float* __restrict__ Ybar, int64_t P,
                                                     uint16_t* __restrict__ YW, uint16_t* __restrict__ YD) {
-  constexpr int NSB = (C + 1) / 2, NP = tc_np(C), N = NP * C, NKB = O / TC_KB;
+  constexpr int NP = tc_np(C), N = NP * C, NKB = O / TC_KB;
   extern __shared__ float ys[];   // [8][C][O]
   const int64_t b = blockIdx.x;
   const int64_t p0 = b * 8;
@@ -394,15 +394,20 @@ __global__ void __launch_bounds__(256) k_split_ybar(const float* __restrict__ Yb
     reinterpret_cast<float4*>(ys)[e] = v;
   }
   __syncthreads();
-  for (int t = threadIdx.x; t < NSB * 2 * O; t += blockDim.x) {
-    const int o = t % O, ch = (t / O) & 1, ss = t / (2 * O);
-    const int c = 2 * ss + ch;
+  // wgrad operand: K chunks of 8 points are packed densely over (block, channel): chunk z = b*C + c
+  // goes to stage z/2, half z%2 (no zero channel for odd C); the chunk after the last block of an odd
+  // total is zero-filled (it pairs with that block's last channel in the final stage).
+  const bool tail = (b == (int64_t)gridDim.x - 1) && ((gridDim.x * (int64_t)C) & 1);
+  for (int t = threadIdx.x; t < (C + (tail ? 1 : 0)) * O; t += blockDim.x) {
+    const int o = t % O, c = t / O;
     float v[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) v[q] = (c < C) ? ys[(q * C + c) * O + o] : 0.f;
     uint4 hi, lo;
     tc::split8_bf16(v, hi, lo);
-    uint16_t* dst = YW + (b * NSB + ss) * (int64_t)(2 * 2 * O * 8);
+    const int64_t z = b * C + c;
+    const int ch = (int)(z & 1);
+    uint16_t* dst = YW + (z >> 1) * (int64_t)(2 * 2 * O * 8);
     *reinterpret_cast<uint4*>(dst + (ch * O + o) * 8) = hi;
     *reinterpret_cast<uint4*>(dst + 2 * O * 8 + (ch * O + o) * 8) = lo;
   }
@@ -519,7 +524,7 @@ hrkan_status tc_split_ybar(hrkan_net* net, int l, const float* Ybar, int64_t n, 
     const int O = net->widths[l + 1];
     const int64_t nb8 = (n + 7) / 8;
     const int64_t ntile = (n + tc_np(C) - 1) / tc_np(C);
-    const size_t yw = (size_t)nb8 * ((C + 1) / 2) * 2 * 2 * O * 8;
+    const size_t yw = (size_t)((nb8 * C + 1) / 2) * 2 * 2 * O * 8;        // densely packed K chunks
     const size_t yd = (size_t)ntile * (O / TC_KB) * 2 * 2 * tc_np(C) * C * 8;
     HR_CUDA(net->tc_yw.ensure(yw * sizeof(uint16_t)));
     HR_CUDA(net->tc_yd.ensure(yd * sizeof(uint16_t)));
