@@ -387,11 +387,19 @@ __global__ void __launch_bounds__(256) k_split_ybar(const float* __restrict__ Yb
   const int64_t b = blockIdx.x;
   const int64_t p0 = b * 8;
   const float4* src = reinterpret_cast<const float4*>(Ybar + p0 * (int64_t)(C * O));
-  for (int e = threadIdx.x; e < 8 * C * O / 4; e += blockDim.x) {
-    const int q = (e * 4) / (C * O);
-    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (p0 + q < P) v = __ldg(src + e);
-    reinterpret_cast<float4*>(ys)[e] = v;
+  constexpr int NV = 8 * C * O / 4;               // float4s of the 8-point block
+  constexpr int UNR = 8;                          // loads in flight per thread (the kernel is HBM-latency bound)
+  for (int e0 = threadIdx.x; e0 < NV; e0 += UNR * 256) {
+    float4 v[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const int e = e0 + u * 256;
+      v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (e < NV && p0 + (e * 4) / (C * O) < P) v[u] = __ldg(src + e);
+    }
+#pragma unroll
+    for (int u = 0; u < UNR; ++u)
+      if (e0 + u * 256 < NV) reinterpret_cast<float4*>(ys)[e0 + u * 256] = v[u];
   }
   __syncthreads();
   // wgrad operand: K chunks of 8 points are packed densely over (block, channel): chunk z = b*C + c
