@@ -383,7 +383,8 @@ template <int C, int O>
 __global__ void __launch_bounds__(256) k_split_ybar(const float* __restrict__ Ybar, int64_t P,
                                                     uint16_t* __restrict__ YW, uint16_t* __restrict__ YD) {
   constexpr int NP = tc_np(C), N = NP * C, NKB = O / TC_KB;
-  extern __shared__ float ys[];   // [8][C][O]
+  constexpr int OS = O + 4;                       // padded row stride: the YD pass reads rows at stride OS
+  extern __shared__ float ys[];                   // [8*C rows = q*C + c][OS]
   const int64_t b = blockIdx.x;
   const int64_t p0 = b * 8;
   const float4* src = reinterpret_cast<const float4*>(Ybar + p0 * (int64_t)(C * O));
@@ -398,19 +399,22 @@ __global__ void __launch_bounds__(256) k_split_ybar(const float* __restrict__ Yb
       if (e < NV && p0 + (e * 4) / (C * O) < P) v[u] = __ldg(src + e);
     }
 #pragma unroll
-    for (int u = 0; u < UNR; ++u)
-      if (e0 + u * 256 < NV) reinterpret_cast<float4*>(ys)[e0 + u * 256] = v[u];
+    for (int u = 0; u < UNR; ++u) {
+      const int e = e0 + u * 256;
+      if (e < NV) reinterpret_cast<float4*>(ys + ((e * 4) / O) * OS)[((e * 4) % O) / 4] = v[u];
+    }
   }
   __syncthreads();
   // wgrad operand: K chunks of 8 points are packed densely over (block, channel): chunk z = b*C + c
   // goes to stage z/2, half z%2 (no zero channel for odd C); the chunk after the last block of an odd
-  // total is zero-filled (it pairs with that block's last channel in the final stage).
+  // total is zero-filled (it pairs with that block's last channel in the final stage).  Lanes run
+  // along o: 16-B stores are contiguous.
   const bool tail = (b == (int64_t)gridDim.x - 1) && ((gridDim.x * (int64_t)C) & 1);
   for (int t = threadIdx.x; t < (C + (tail ? 1 : 0)) * O; t += blockDim.x) {
     const int o = t % O, c = t / O;
     float v[8];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) v[q] = (c < C) ? ys[(q * C + c) * O + o] : 0.f;
+    for (int q = 0; q < 8; ++q) v[q] = (c < C) ? ys[(q * C + c) * OS + o] : 0.f;
     uint4 hi, lo;
     tc::split8_bf16(v, hi, lo);
     const int64_t z = b * C + c;
@@ -419,19 +423,21 @@ __global__ void __launch_bounds__(256) k_split_ybar(const float* __restrict__ Yb
     *reinterpret_cast<uint4*>(dst + (ch * O + o) * 8) = hi;
     *reinterpret_cast<uint4*>(dst + 2 * O * 8 + (ch * O + o) * 8) = lo;
   }
+  // dgrad operand: lanes run along the 8*C rows (p*C + c) of this block, which are contiguous rows
+  // of the tile's N -- 16-B stores are contiguous (the row-fastest order also keeps the float4 reads
+  // of the padded smem rows conflict-free).
+  const int64_t tile = p0 / NP;
+  const int row0 = (int)(p0 - tile * NP) * C;
   for (int t = threadIdx.x; t < 8 * C * (O / 8); t += blockDim.x) {
-    const int og = t % (O / 8), c = (t / (O / 8)) % C, q = t / ((O / 8) * C);
-    const int64_t p = p0 + q;
-    const int64_t tile = p / NP;
-    const int row = (int)(p - tile * NP) * C + c;
-    float v[8];
-#pragma unroll
-    for (int e = 0; e < 8; ++e) v[e] = ys[(q * C + c) * O + og * 8 + e];
+    const int rw = t % (8 * C), og = t / (8 * C);
+    const float4* sp = reinterpret_cast<const float4*>(ys + rw * OS + og * 8);
+    const float4 a0 = sp[0], a1 = sp[1];
+    float v[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
     uint4 hi, lo;
     tc::split8_bf16(v, hi, lo);
     uint16_t* dst = YD + (tile * NKB + og / 2) * (int64_t)(2 * 2 * N * 8);
-    *reinterpret_cast<uint4*>(dst + ((og & 1) * N + row) * 8) = hi;
-    *reinterpret_cast<uint4*>(dst + 2 * N * 8 + ((og & 1) * N + row) * 8) = lo;
+    *reinterpret_cast<uint4*>(dst + ((og & 1) * N + row0 + rw) * 8) = hi;
+    *reinterpret_cast<uint4*>(dst + 2 * N * 8 + ((og & 1) * N + row0 + rw) * 8) = lo;
   }
 }
 
@@ -539,7 +545,7 @@ hrkan_status tc_split_ybar(hrkan_net* net, int l, const float* Ybar, int64_t n, 
     auto launch = [&](auto OC) -> hrkan_status {
       constexpr int OO = decltype(OC)::value;
       auto kfn = k_split_ybar<C, OO>;
-      constexpr int smem = 8 * C * OO * 4;
+      constexpr int smem = 8 * C * (OO + 4) * 4;
       if (smem > 48 * 1024) HR_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
       HR_LAUNCH(HRKAN_K_OTHER, "k_split_ybar",
                 kfn<<<(unsigned)nb8, 256, smem, st>>>(Ybar, n, (uint16_t*)net->tc_yw.p, (uint16_t*)net->tc_yd.p));
