@@ -199,22 +199,30 @@ __global__ void __launch_bounds__(32 * LF_WARPS)
   }
 }
 
-// dW[t] += sum_b part[b][t] (t < IB), db += sum_b part[b][IB], out_loss += scale * sum_b part[b][IB+1]
-// (double), out_flag += sum_b part[b][IB+2]; every sum in a fixed order.
-__global__ void k_reduce_last(const float* __restrict__ part, int nb, int IB, float* __restrict__ dW,
-                              float* __restrict__ db, float scale, float* __restrict__ out_loss,
-                              float* __restrict__ out_flag) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t < IB) {
-    float s = 0.f;
-    for (int b = 0; b < nb; ++b) s += part[(size_t)b * (IB + 4) + t];
-    dW[t] += s;
-  } else if (t < IB + 3) {
-    double s = 0.0;
-    for (int b = 0; b < nb; ++b) s += (double)part[(size_t)b * (IB + 4) + t];
-    if (t == IB) *db += (float)s;
-    else if (t == IB + 1) *out_loss += (float)(s * (double)scale);
-    else *out_flag += (float)s;
+// dW[t] += sum_b part[b][t] (t < IB), db += sum_b part[b][IB], out_loss += scale * sum_b part[b][IB+1],
+// out_flag += sum_b part[b][IB+2].  A block of 256 threads takes 32 columns; its 8 warps sum the
+// blocks b = g (mod 8) (8 independent chains, coalesced 128-B rows) in double, and warp 0 adds the 8
+// chains in order: every sum is in a fixed order (bitwise reproducible for a fixed grid).
+constexpr int RL_COLS = 32, RL_CHAINS = 8;
+__global__ void __launch_bounds__(RL_COLS * RL_CHAINS)
+    k_reduce_last(const float* __restrict__ part, int nb, int IB, float* __restrict__ dW, float* __restrict__ db,
+                  float scale, float* __restrict__ out_loss, float* __restrict__ out_flag) {
+  __shared__ double sh[RL_CHAINS][RL_COLS];
+  const int lane = threadIdx.x & (RL_COLS - 1), g = threadIdx.x / RL_COLS;
+  const int t = blockIdx.x * RL_COLS + lane;
+  double s = 0.0;
+  if (t < IB + 3)
+    for (int b = g; b < nb; b += RL_CHAINS) s += (double)__ldg(part + (size_t)b * (IB + 4) + t);
+  sh[g][lane] = s;
+  __syncthreads();
+  if (g == 0 && t < IB + 3) {
+    double v = 0.0;
+#pragma unroll
+    for (int k = 0; k < RL_CHAINS; ++k) v += sh[k][lane];
+    if (t < IB) dW[t] += (float)v;
+    else if (t == IB) *db += (float)v;
+    else if (t == IB + 1) *out_loss += (float)(v * (double)scale);
+    else *out_flag += (float)v;
   }
 }
 
@@ -229,6 +237,28 @@ __global__ void k_reduce_last(const float* __restrict__ part, int nb, int IB, fl
 //   pass 2   per point, dW contributions and the input-jet adjoint Xbar (same formulas as above).
 // ---------------------------------------------------------------------------------------------
 constexpr int LV_PB = 4;
+
+// Transposing warp sum of NV values per lane (NV a power of two <= 32): at each step of width h the
+// lanes with bit h set keep the upper half of their values and send the lower half (and vice versa),
+// so NV - 1 shuffles replace 5*NV; the remaining butterflies (h >= NV) finish the sum.  Afterwards
+// lane l holds the warp total of value l % NV.  Fixed order: deterministic.
+template <int NV>
+__device__ __forceinline__ float warp_sum_transpose(float (&V)[NV], int lane) {
+#pragma unroll
+  for (int h = NV / 2; h >= 1; h >>= 1) {
+    const bool up = (lane & h) != 0;
+#pragma unroll
+    for (int k = 0; k < h; ++k) {
+      const float send = up ? V[k] : V[k + h];
+      const float keep = up ? V[k + h] : V[k];
+      V[k] = keep + __shfl_xor_sync(0xffffffffu, send, h);
+    }
+  }
+  float r = V[0];
+#pragma unroll
+  for (int h = NV; h < 32; h <<= 1) r += __shfl_xor_sync(0xffffffffu, r, h);
+  return r;
+}
 
 template <int NF, int NS, int M, int MODE>
 __global__ void __launch_bounds__(256, 3)
@@ -276,8 +306,17 @@ __global__ void __launch_bounds__(256, 3)
           for (int c = 0; c < C; ++c) jw[(q * C + c) * 32] = v[q][c];
         }
     }
-#pragma unroll 1
-    for (int q = 0; q < npb; ++q) {
+    // pass 1: the warp's partial jets of all batch points, then ONE transposing butterfly over the
+    // LV_PB*C values (log2 NV exchange steps of halving width instead of 5 per value)
+    constexpr int NVT = LV_PB * C;
+    constexpr int NV = NVT <= 4 ? 4 : NVT <= 8 ? 8 : NVT <= 16 ? 16 : 32;
+    static_assert(NVT <= 32, "batch x channels must fit one warp");
+    float V[NV];
+#pragma unroll
+    for (int k = 0; k < NV; ++k) V[k] = 0.f;
+#pragma unroll
+    for (int q = 0; q < LV_PB; ++q) {
+      if (q >= npb) break;
       const float* jq = jw + q * C * 32;
       const float x = jq[0];
       float s[C];
@@ -307,14 +346,11 @@ __global__ void __launch_bounds__(256, 3)
         s[1 + NF + a] = fmaf(T2 * d1, d1, T1 * d2);
       }
 #pragma unroll
-      for (int c = 0; c < C; ++c) {
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) s[c] += __shfl_xor_sync(0xffffffffu, s[c], o);
-      }
-      if (lane == 0) {
-#pragma unroll
-        for (int c = 0; c < C; ++c) wpart[(q * nw + warp) * C + c] = s[c];
-      }
+      for (int c = 0; c < C; ++c) V[q * C + c] = s[c];
+    }
+    {
+      const float tot = warp_sum_transpose<NV>(V, lane);   // lane l: warp total of value l % NV
+      if (lane < NVT && lane / C < npb) wpart[((lane / C) * nw + warp) * C + lane % C] = tot;
     }
     __syncthreads();
     // ---------------- totals, residual, loss, seeds (thread q per point)

@@ -51,7 +51,7 @@ hrkan_status launch_last(hrkan_net* net, const float* in, int64_t n, const PassA
                                       xbar, net->last_part.f(), pbm));
     const float scale = (MODE == LAST_BOUNDARY) ? a.inv_n : pde->alpha * a.inv_n;
     HR_LAUNCH(HRKAN_K_REDUCE, "k_reduce_last",
-              k_reduce_last<<<(IB + 3 + 255) / 256, 256, 0, st>>>(net->last_part.f(), nb, IB, a.grad + net->w_off[l],
+              k_reduce_last<<<(IB + 3 + RL_COLS - 1) / RL_COLS, RL_COLS * RL_CHAINS, 0, st>>>(net->last_part.f(), nb, IB, a.grad + net->w_off[l],
                                                                    a.grad + net->b_off[l], scale, a.out_loss, a.out_flag));
     return HRKAN_OK;
   }
@@ -81,7 +81,7 @@ hrkan_status launch_last(hrkan_net* net, const float* in, int64_t n, const PassA
                                                  pde->visc, a.inv_n, xbar, net->last_part.f()));
   const float scale = (MODE == LAST_BOUNDARY) ? a.inv_n : pde->alpha * a.inv_n;
   HR_LAUNCH(HRKAN_K_REDUCE, "k_reduce_last",
-            k_reduce_last<<<(IB + 3 + 255) / 256, 256, 0, st>>>(net->last_part.f(), nb, IB, a.grad + net->w_off[l],
+            k_reduce_last<<<(IB + 3 + RL_COLS - 1) / RL_COLS, RL_COLS * RL_CHAINS, 0, st>>>(net->last_part.f(), nb, IB, a.grad + net->w_off[l],
                                                                  a.grad + net->b_off[l], scale, a.out_loss, a.out_flag));
   return HRKAN_OK;
 }

@@ -602,7 +602,7 @@ hrkan_status launch_wgrad_tc(hrkan_net* net, int l, const float* X, const float*
   const int nz = (int)std::min<int64_t>(1024, std::max<int64_t>(1, n / 256));
   HR_LAUNCH(HRKAN_K_REDUCE, "k_bias_part",
             k_bias_part<<<dim3((O + 127) / 128, nz), 128, 0, st>>>(Ybar, C, O, n, part_b));
-  HR_LAUNCH(HRKAN_K_REDUCE, "k_reduce_bias", k_reduce_bias<<<(O + 127) / 128, 128, 0, st>>>(part_b, nz, O, db));
+  HR_LAUNCH(HRKAN_K_REDUCE, "k_reduce_bias", k_reduce_bias<<<(O + 31) / 32, 256, 0, st>>>(part_b, nz, O, db));
   return HRKAN_OK;
 }
 
