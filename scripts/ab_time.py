@@ -15,11 +15,14 @@ ap = argparse.ArgumentParser()
 ap.add_argument("keys", nargs="*", default=["C5", "C4", "C3"])
 ap.add_argument("--n", type=int, default=1 << 18)
 ap.add_argument("--reps", type=int, default=5)
+ap.add_argument("--m", type=int, default=0, help="override the HR order m (0: the workload's)")
+ap.add_argument("--engine", type=int, default=0, help="0 auto, 1 band-limited SIMT, 2 tensor cores")
 a = ap.parse_args()
 tag = os.path.basename(os.path.dirname(os.environ.get("HRKAN_LIB", "/base/x")))
 for key in a.keys:
     w = HI.WORKLOADS[key]
-    net = HRKANNet(w.widths, w.G, w.k, w.m, seed=HI.PARAM_SEED)
+    net = HRKANNet(w.widths, w.G, w.k, a.m or w.m, seed=HI.PARAM_SEED)
+    net.set_engine(a.engine)
     g = torch.Generator(device="cpu").manual_seed(1)
     pts = (torch.rand(a.n, w.D, generator=g) * 2 - 1).cuda()
     if w.pde == "burgers":
@@ -45,4 +48,4 @@ for key in a.keys:
         for k, v in pr.items():
             cls.setdefault(k, []).append(v[0])
     med = {k: round(statistics.median(v), 3) for k, v in cls.items() if statistics.median(v) > 0.05}
-    print(f"{tag:10s} {key} total {statistics.median(tot):.3f} ms", med, flush=True)
+    print(f"{tag:10s} {key} m={a.m or w.m} eng={a.engine} total {statistics.median(tot):.3f} ms", med, flush=True)
