@@ -461,7 +461,7 @@ def main():
             hit = [v for v in tj["kernels"].values() if v.get("class") == dominant]
             if hit and dom_n:
                 pts_per_launch = (len(sh.interior) + sh.n_bi) * prof_steps / dom_n
-                traffic = hit[0]["dram_bytes_per_point"] * pts_per_launch
+                traffic = max(hit, key=lambda v: v["time_ms"])["dram_bytes_per_point"] * pts_per_launch
                 traffic_note = "ncu dram bytes/point (profiles/r01_ncu_c5.json) x points per launch"
     except (OSError, ValueError, KeyError):
         pass

@@ -1,0 +1,77 @@
+"""Summarise an `ncu --set full` report of scripts/prof_step.py into profiles/rNN_ncu_<cfg>.json (read by
+bench.py for the roofline `traffic` field) and a markdown table.
+
+    python scripts/ncu_summary.py report.ncu-rep C5 65536 profiles/r01_ncu_c5   # writes .json and _summary.md
+"""
+import csv
+import io
+import json
+import re
+import subprocess
+import sys
+
+CLASS = [("k_fwd_first", "fwd_first"), ("k_fwd_tc", "fwd_hidden"), ("k_fwd_simt", "fwd_hidden"),
+         ("k_last", "fwd_last"), ("k_wgrad_first", "wgrad_first"), ("k_wgrad_tc", "wgrad_hidden"),
+         ("k_wgrad_simt", "wgrad_hidden"), ("k_dgrad", "dgrad_hidden"), ("k_reduce", "reduce"),
+         ("k_bias_part", "reduce"), ("k_adam", "adam"), ("k_tiny_step", "fused_step")]
+
+
+def main():
+    rep, cfg, npts, out = sys.argv[1], sys.argv[2], int(sys.argv[3]), sys.argv[4]
+    txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(txt)))
+    hdr = rows[0]
+    ix = {h: i for i, h in enumerate(hdr)}
+
+    def val(r, k):
+        try:
+            return float(r[ix[k]].replace(",", ""))
+        except (KeyError, ValueError):
+            return None
+
+    kernels = {}
+    for r in rows[2:]:
+        name = r[ix["Kernel Name"]]
+        m = re.search(r"(k_\w+)(<[^>]*>)?", name)
+        if not m:
+            continue
+        short = m.group(1) + (m.group(2) or "")
+        cls = next((c for p, c in CLASS if m.group(1).startswith(p)), "other")
+        def nbytes(k):
+            v = val(r, k)
+            if v is None:
+                return None
+            u = rows[1][ix[k]].lower()
+            return v * {"byte": 1.0, "kbyte": 1e3, "mbyte": 1e6, "gbyte": 1e9, "kb": 1e3, "mb": 1e6, "gb": 1e9}.get(u, 1.0)
+
+        rd, wr = nbytes("dram__bytes_read.sum"), nbytes("dram__bytes_write.sum")
+        t_unit = rows[1][ix["gpu__time_duration.sum"]]
+        t = val(r, "gpu__time_duration.sum")
+        t_ms = t / 1e6 if t_unit == "ns" else t / 1e3 if t_unit in ("us", "usecond") else t
+        entry = {"class": cls, "time_ms": t_ms,
+                 "tensor_pipe_pct": val(r, "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed") or 0.0,
+                 "issue_active_pct": val(r, "smsp__issue_active.avg.pct_of_peak_sustained_active"),
+                 "lts_pct": val(r, "lts__t_sectors.avg.pct_of_peak_sustained_elapsed"),
+                 "dram_read_bytes": rd, "dram_write_bytes": wr,
+                 "sm_clock_ghz": val(r, "sm__cycles_elapsed.avg.per_second")}
+        entry["dram_bytes_per_point"] = ((entry["dram_read_bytes"] or 0) + (entry["dram_write_bytes"] or 0)) / npts
+        if short not in kernels or kernels[short]["time_ms"] < t_ms:   # keep the interior (largest) launch
+            kernels[short] = entry
+    js = {"workload": cfg,
+          "capture": f"ncu --set full --clock-control none, scripts/prof_step.py {cfg} {npts} 1 "
+                     f"(interior pass, {npts} points, one launch per kernel)",
+          "points_per_capture": npts, "kernels": kernels}
+    json.dump(js, open(out + ".json", "w"), indent=1)
+    lines = [f"# ncu summary, {cfg} (interior pass, {npts} points; `ncu --set full --clock-control none`)", "",
+             "| kernel | time ms | tensor pipe % | issue % | L2 % | DRAM B/point | SM GHz |", "|---|---|---|---|---|---|---|"]
+    for k, e in sorted(kernels.items(), key=lambda kv: -kv[1]["time_ms"]):
+        if e["time_ms"] < 0.005:
+            continue
+        lines.append(f"| `{k}` | {e['time_ms']:.3f} | {e['tensor_pipe_pct']:.1f} | {e['issue_active_pct'] or 0:.1f} | "
+                     f"{e['lts_pct'] or 0:.1f} | {e['dram_bytes_per_point']:.0f} | {e['sm_clock_ghz'] or 0:.2f} |")
+    open(out + "_summary.md", "w").write("\n".join(lines) + "\n")
+    print("\n".join(lines))
+
+
+if __name__ == "__main__":
+    main()
