@@ -250,9 +250,14 @@ __global__ void __launch_bounds__(DgrCfg<NF, NS, M, OO>::THREADS, 1)
     // epilogue, so the MMA is only held back by the TMEM accumulators it releases early
     if (lane == 0) {
       const uint16_t* ytile = Ysplit + (int64_t)blockIdx.x * NKB * (Cfg::Y_STAGE_BYTES / 2);
+#ifndef HRKAN_DGR_PREFETCH
+#define HRKAN_DGR_PREFETCH 0
+#endif
       for (int g = 0; g < nblk; ++g) {
         const int kb = g - (g / NKB) * NKB;
         const int s = g % NSTAGE;
+        if (HRKAN_DGR_PREFETCH > 0 && g + HRKAN_DGR_PREFETCH < NKB)   // first M-tile pass streams Ybar from HBM
+          tc::bulk_prefetch_l2(ytile + (int64_t)(g + HRKAN_DGR_PREFETCH) * (Cfg::Y_STAGE_BYTES / 2), Cfg::Y_STAGE_BYTES);
         tc::mbar_wait(&empty_bar[s], ((g / NSTAGE) & 1) ^ 1);
         tc::mbar_arrive_expect_tx(&full_bar[s], Cfg::STAGE_BYTES);
         tc::bulk_g2s(smem + s * Cfg::STAGE_BYTES, Wtiled + (int64_t)g * (Cfg::W_STAGE_BYTES / 2), Cfg::W_STAGE_BYTES,

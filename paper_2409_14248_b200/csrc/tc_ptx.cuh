@@ -67,6 +67,11 @@ __device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src_gmem, u
                : "memory");
 }
 
+// L2 prefetch of a contiguous global range (16-B aligned, multiple of 16 bytes); no completion.
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src_gmem, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src_gmem), "r"(bytes) : "memory");
+}
+
 // ------------------------------------------------------------------ TMA tensor copy global -> smem
 // 3-D tiled box (coordinates innermost first); out-of-bounds elements are zero-filled and still
 // count towards the transaction bytes.
