@@ -492,10 +492,10 @@ template <int NF, int NS, int M, int OO>
 hrkan_status launch_fwd_tc(hrkan_net* net, int l, const float* X, float* Y, int64_t n, cudaStream_t st) {
   using Cfg = FwdCfg<NF, NS, M, OO>;
   auto kfn = k_fwd_tc<NF, NS, M, OO>;
-  static bool attr_set = false;
-  if (!attr_set) {
+  static uint64_t attr_dev = 0;                   // function attributes are per device (context)
+  if (!((attr_dev >> (net->device & 63)) & 1)) {
     HR_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
-    attr_set = true;
+    attr_dev |= 1ull << (net->device & 63);
   }
   const int I = net->widths[l];
   CUtensorMap tm;
@@ -563,10 +563,10 @@ hrkan_status launch_wgrad_tc(hrkan_net* net, int l, const float* X, const float*
   using Cfg = WgrCfg<NF, NS, M, OO>;
   constexpr int C = Cfg::C, O = Cfg::O;
   auto kfn = k_wgrad_tc<NF, NS, M, OO>;
-  static bool attr_set = false;
-  if (!attr_set) {
+  static uint64_t attr_dev = 0;                   // function attributes are per device (context)
+  if (!((attr_dev >> (net->device & 63)) & 1)) {
     HR_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
-    attr_set = true;
+    attr_dev |= 1ull << (net->device & 63);
   }
   const int I = net->widths[l];
   const int64_t K = (int64_t)I * net->B;
@@ -624,10 +624,10 @@ hrkan_status launch_dgrad_tc(hrkan_net* net, int l, const float* X, const float*
                              cudaStream_t st) {
   using Cfg = DgrCfg<NF, NS, M, OO>;
   auto kfn = k_dgrad_tc<NF, NS, M, OO>;
-  static bool attr_set = false;
-  if (!attr_set) {
+  static uint64_t attr_dev = 0;                   // function attributes are per device (context)
+  if (!((attr_dev >> (net->device & 63)) & 1)) {
     HR_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
-    attr_set = true;
+    attr_dev |= 1ull << (net->device & 63);
   }
   const TcLayerState& ls = net->tc_layers[l];
   const int I = net->widths[l];
