@@ -162,16 +162,44 @@ __device__ __forceinline__ void tiny_point(const TinyNet& tn, const float* __res
           g2 = fmaf(yb[o][1 + NF + a] * dx[a], dx[a], g2);
         }
         float T1 = 0.f, T2 = 0.f, T3 = 0.f;
-        // dW[o, i, n] for every n (warp-uniform index), band contributions only
-        for (int n = 0; n < B; ++n) {
-          const int rr = n - n0;
-          float v0 = 0.f, v1 = 0.f, v2 = 0.f;
+        // dW[o, i, n] for every n: the lane's k+1 band contributions placed at n0 + rr, then ONE
+        // transposing butterfly over the B (<= 16) values -- lane n ends with the warp total of basis n
+        float cr[KMAX];
 #pragma unroll
-          for (int q = 0; q < KMAX; ++q)
-            if (q == rr) { v0 = vv[0][q]; v1 = vv[1][q]; v2 = vv[2][q]; }
-          const float contrib = fmaf(yb[o][0], v0, fmaf(g1, v1, g2 * v2));
-          const float s = warp_sum(contrib);
-          if (lane == 0) gw[tn.woff[l] + (o * I + i) * B + n] += s;
+        for (int rr = 0; rr < KMAX; ++rr) cr[rr] = fmaf(yb[o][0], vv[0][rr], fmaf(g1, vv[1][rr], g2 * vv[2][rr]));
+        float* gdst = gw + tn.woff[l] + (o * I + i) * B;
+        if (B <= 8) {
+          float V[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            float v = 0.f;
+#pragma unroll
+            for (int rr = 0; rr < KMAX; ++rr) v = (rr <= bc.k && q - rr == n0) ? cr[rr] : v;
+            V[q] = v;
+          }
+          const float tot = warp_sum_transpose<8>(V, lane);
+          if (lane < B) gdst[lane] += tot;
+        } else if (B <= 16) {
+          float V[16];
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            float v = 0.f;
+#pragma unroll
+            for (int rr = 0; rr < KMAX; ++rr) v = (rr <= bc.k && q - rr == n0) ? cr[rr] : v;
+            V[q] = v;
+          }
+          const float tot = warp_sum_transpose<16>(V, lane);
+          if (lane < B) gdst[lane] += tot;
+        } else {
+          for (int n = 0; n < B; ++n) {
+            const int rr = n - n0;
+            float c = 0.f;
+#pragma unroll
+            for (int q = 0; q < KMAX; ++q)
+              if (q == rr) c = cr[q];
+            const float sw = warp_sum(c);
+            if (lane == 0) gdst[n] += sw;
+          }
         }
         if (l > 0) {
 #pragma unroll
