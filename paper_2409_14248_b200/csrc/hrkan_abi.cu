@@ -496,7 +496,7 @@ void hrkan_free(hrkan_net_t net) {
   DevBuf* bufs[] = {&net->jets, &net->adj_a, &net->adj_b, &net->loss_part, &net->w_part, &net->b_part, &net->last_part, &net->first_part,
                     &net->st_int, &net->st_f, &net->st_bnd, &net->st_gb, &net->st_ini, &net->st_gi,
                     &net->st_out, &net->st_pts, &net->st_u, &net->st_du, &net->st_d2u, &net->tc_ws,
-                    &net->tc_yw, &net->tc_yd};
+                    &net->tc_yw, &net->tc_yd, &net->tiny_cnt};
   for (DevBuf* b : bufs) b->release();
   tc_free(net);
   delete net;

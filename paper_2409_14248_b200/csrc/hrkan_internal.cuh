@@ -129,6 +129,7 @@ struct hrkan_net {
   DevBuf jets, adj_a, adj_b, loss_part, w_part, b_part, last_part, first_part;
   DevBuf st_int, st_f, st_bnd, st_gb, st_ini, st_gi, st_out, st_pts, st_u, st_du, st_d2u;
   DevBuf tc_ws;                         // tensor-core path scratch
+  DevBuf tiny_cnt;                      // k_tiny_step's finished-block counter (reset by the last block)
   DevBuf tc_yw, tc_yd;                  // pre-split bf16 hi/lo Ybar operands of the reverse kernels
   std::vector<TcLayerState> tc_layers;
   int tc_seg = 96;                      // K-blocks per forward TMEM segment, double-buffered accumulators (C3/C4: one segment;

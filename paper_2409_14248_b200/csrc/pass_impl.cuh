@@ -240,6 +240,10 @@ hrkan_status run_tiny(hrkan_net* net, const TinyArgs& t, cudaStream_t st) {
   const int nb_ini = (int)((t.N0 + TINY_THREADS - 1) / TINY_THREADS);
   const int nb = std::max(1, nb_int + nb_bnd + nb_ini);
   HR_CUDA(net->last_part.ensure(sizeof(float) * (size_t)nb * (tn.np + 4)));
+  if (!net->tiny_cnt.p) {                          // first call is never captured (graph mode captures the 2nd)
+    HR_CUDA(net->tiny_cnt.ensure(sizeof(unsigned)));
+    HR_CUDA(cudaMemsetAsync(net->tiny_cnt.p, 0, sizeof(unsigned), st));
+  }
   const hrkan_pde* pde = t.pde;
   auto go = [&](auto NFc, auto NSc, auto BUR) -> hrkan_status {
     constexpr int NF = decltype(NFc)::value, NS = decltype(NSc)::value;
@@ -248,16 +252,13 @@ hrkan_status run_tiny(hrkan_net* net, const TinyArgs& t, cudaStream_t st) {
               (k_tiny_step<NF, NS, M, BURGERS><<<nb, TINY_THREADS, 0, st>>>(
                   tn, net->params, net->bc, net->D, t.interior, t.forcing, t.Ni, nb_int, t.boundary, t.g_boundary, t.Nb,
                   nb_bnd, t.initial, t.g_initial, t.N0, pde->alpha, pde->adv, pde->visc, t.inv_int, t.inv_bi,
-                  net->last_part.f())));
+                  net->last_part.f(), (unsigned*)net->tiny_cnt.p, pde->alpha * t.inv_int, t.out)));
     return HRKAN_OK;
   };
   if (pde->kind == HRKAN_BURGERS) HR_TRY(go(IC<2>{}, IC<1>{}, std::true_type{}));
   else if (net->D == 1) HR_TRY(go(IC<1>{}, IC<1>{}, std::false_type{}));
   else if (net->D == 2) HR_TRY(go(IC<2>{}, IC<2>{}, std::false_type{}));
   else HR_TRY(go(IC<3>{}, IC<3>{}, std::false_type{}));
-  HR_LAUNCH(HRKAN_K_REDUCE, "k_tiny_reduce",
-            k_tiny_reduce<<<(tn.np + 4 + 255) / 256, 256, 0, st>>>(net->last_part.f(), nb, tn.np,
-                                                                   pde->alpha * t.inv_int, t.inv_bi, t.out));
   return HRKAN_OK;
 }
 

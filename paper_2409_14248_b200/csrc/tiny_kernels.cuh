@@ -8,7 +8,7 @@
 // P:195-236), band-limited to the k+1 bases that are non-zero at each x.  Gradients are reduced
 // deterministically: per parameter a warp butterfly (all lanes see the same parameter index; lanes
 // whose band misses it add 0), per-warp slots in shared memory, a fixed-order block sum into
-// part[block][np + 4] and k_tiny_reduce over the blocks.  Blocks [0, nb_int) take interior points,
+// part[block][np + 4], summed over the blocks in order by the last block to finish.  Blocks [0, nb_int) take interior points,
 // the rest boundary then initial points (value-only, C = 1), so a block never mixes modes.
 #pragma once
 
@@ -245,7 +245,8 @@ __global__ void __launch_bounds__(TINY_THREADS)
                 const float* __restrict__ interior, const float* __restrict__ forcing, int64_t Ni, int nb_int,
                 const float* __restrict__ boundary, const float* __restrict__ gb, int64_t Nb, int nb_bnd,
                 const float* __restrict__ initial, const float* __restrict__ gi, int64_t N0,
-                float alpha, float adv, float visc, float inv_int, float inv_bi, float* __restrict__ part) {
+                float alpha, float adv, float visc, float inv_int, float inv_bi, float* __restrict__ part,
+                unsigned* __restrict__ done, float s_int, float* __restrict__ out) {
   __shared__ float prm[TINY_MAXP];
   __shared__ float gws[TINY_THREADS / 32][TINY_MAXP];
   const int np = tn.np;
@@ -308,24 +309,30 @@ __global__ void __launch_bounds__(TINY_THREADS)
     for (int w = 0; w < TINY_THREADS / 32; ++w) v += red[threadIdx.x][w];
     dst[np + threadIdx.x] = v;
   }
-}
-
-// out[t] = sum_b part[b][t] (fixed order); out[np] = alpha/N_int * sum r^2, out[np+1] = 1/N_bi * sum e^2
-// (double accumulation), out[np+2] = non-finite count, out[np+3] = 0.  Overwrites out.
-__global__ void k_tiny_reduce(const float* __restrict__ part, int nb, int np, float s_int, float s_bi,
-                              float* __restrict__ out) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t < np) {
-    float s = 0.f;
-    for (int b = 0; b < nb; ++b) s += part[(size_t)b * (np + 4) + t];
-    out[t] = s;
-  } else if (t < np + 4) {
-    double s = 0.0;
-    if (t < np + 3)
-      for (int b = 0; b < nb; ++b) s += (double)part[(size_t)b * (np + 4) + t];
-    const double sc = (t == np) ? (double)s_int : (t == np + 1) ? (double)s_bi : 1.0;
-    out[t] = (t == np + 3) ? 0.f : (float)(s * sc);
+  // the last block to finish sums every block's partials in block order (deterministic) -- the
+  // whole loss + gradient is one launch
+  __shared__ unsigned ticket;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) ticket = atomicAdd(done, 1u);
+  __syncthreads();
+  if (ticket != gridDim.x - 1) return;
+  __threadfence();
+  const int nb = (int)gridDim.x;
+  for (int t = threadIdx.x; t < np + 4; t += blockDim.x) {
+    if (t < np) {
+      float sv = 0.f;
+      for (int bb = 0; bb < nb; ++bb) sv += __ldcg(part + (size_t)bb * (np + 4) + t);
+      out[t] = sv;
+    } else {
+      double sv = 0.0;
+      if (t < np + 3)
+        for (int bb = 0; bb < nb; ++bb) sv += (double)__ldcg(part + (size_t)bb * (np + 4) + t);
+      const double sc = (t == np) ? (double)s_int : (t == np + 1) ? (double)inv_bi : 1.0;
+      out[t] = (t == np + 3) ? 0.f : (float)(sv * sc);
+    }
   }
+  if (threadIdx.x == 0) *done = 0u;                // ready for the next call (and graph replay)
 }
 
 }  // namespace
