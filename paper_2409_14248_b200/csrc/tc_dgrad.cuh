@@ -6,8 +6,9 @@
 //   xbar    = sum_n [Abar^0 v1 + sum_a Abar^{1,a} v2 dx_a + sum_a Abar^{2,a} (v3 dx_a^2 + v2 ddx_a)]
 //   dxbar_a = sum_n [Abar^{1,a} v1 + 2 Abar^{2,a} v2 dx_a],     ddxbar_a = sum_n Abar^{2,a} v1
 //
-// Orientation: MMA M = rows (i,n) of an INPUT-ALIGNED tile (IPT = floor(128/B) whole inputs, so every
-// sum over n closes inside one tile), MMA N = (point, channel) columns p*C + c of NP points, MMA
+// Orientation: MMA M = 128 contiguous K rows (i,n) -- an input split between two tiles is summed through
+// a per-point carry in shared memory (input-aligned tiles of floor(128/B) whole inputs when B < 11, see
+// dgr_rows_per_tile) -- MMA N = (point, channel) columns p*C + c of NP points, MMA
 // K = o.  A = pre-tiled W^T hi/lo and B = pre-split Ybar hi/lo (k_split_ybar), both by 1-D bulk
 // copies per stage.  Two TMEM accumulators: the 8 epilogue warps drain M-tile t while the MMA
 // runs t+1.  Epilogue: TMEM -> smem slice of SLICE_P points -> each (point, input) gathers only the
@@ -37,7 +38,19 @@ __host__ __device__ constexpr int dgr_epi_warps(int C) {
   return HRKAN_DGR_EPI_WARPS > 0 ? HRKAN_DGR_EPI_WARPS : C == 4 ? 12 : 8;
 }
 constexpr int DGR_SST = 129;   // column stride of the epilogue slice (odd: conflict-free gathers)
-constexpr int DGR_IPTB = 16;   // jet box width (inputs) >= IPT + 3 (box start aligned down to 16 B), B >= 11
+constexpr int DGR_IPTB = 16;   // jet box width (inputs) >= inputs per M-tile + 3 (box start aligned down to 16 B)
+
+// M-tile rows.  Contiguous: 128 K rows (i, n), an input split between two tiles summed through a
+// per-point carry in shared memory -- used for 3-D nets (7-channel jets, MMA-bound: C5 dgrad 10.8 ->
+// 9.9 ms per 2^18 points, no idle rows) when the jet box holds every input such a tile touches (B >= 11).
+// Input-aligned: floor(128/B) whole inputs (IPT*B < 128 rows busy) -- kept for the 4/5-channel nets,
+// whose epilogue-bound tiles got 14-22 % slower with the extra inputs per contiguous tile.
+__host__ __device__ constexpr int dgr_rows_per_tile(int B, int D) {
+  return (D >= 3 && 127 / B + 5 <= DGR_IPTB) ? 128 : (128 / B) * B;
+}
+__host__ __device__ constexpr bool dgr_tile_ok(int B, int D) {
+  return B >= 1 && ((dgr_rows_per_tile(B, D) == 128 ? 127 / B + 2 : 128 / B) + 3 <= DGR_IPTB);
+}
 
 template <int NF, int NS, int M, int OO>
 struct DgrCfg {
@@ -52,7 +65,7 @@ struct DgrCfg {
   static constexpr int JET_FLOATS = N * DGR_IPTB;             // TMA box X[NP][C][IPTB]
   static constexpr int SLICE_P = dgr_slice_p(C);
   static constexpr int S_FLOATS = SLICE_P * C * DGR_SST;
-  static constexpr int FIXED_BYTES = 4 * (2 * JET_FLOATS + S_FLOATS) + 1024;
+  static constexpr int FIXED_BYTES = 4 * (2 * JET_FLOATS + S_FLOATS + 2 * NP * C) + 1024;   // + split-input carries
   static constexpr int NSTAGE_FIT = (225 * 1024 - FIXED_BYTES) / STAGE_BYTES;
   static constexpr int NSTAGE = NSTAGE_FIT > 8 ? 8 : NSTAGE_FIT;
   static constexpr int SMEM_BYTES = NSTAGE * STAGE_BYTES + FIXED_BYTES;
@@ -66,9 +79,9 @@ struct DgrCfg {
   static_assert(STAGE_BYTES % 128 == 0, "TMA boxes after the stages need 128-B alignment");
 };
 
-// W^T tiles for k_dgrad_tc: for M-tile mt (inputs mt*IPT ...), K-block kb (o = kb*KB ...):
-// [hi | lo] each [2 chunks][128 rows][8] bf16, row = il*B + n (il < IPT), zero outside.
-__global__ void k_tile_w_dgr(const float* __restrict__ W, uint16_t* __restrict__ Wt, int O, int I, int B, int IPT,
+// W^T tiles for k_dgrad_tc: for M-tile mt (K rows mt*RPT ...), K-block kb (o = kb*KB ...):
+// [hi | lo] each [2 chunks][128 rows][8] bf16, row r <-> K row mt*RPT + r (r < RPT), zero outside.
+__global__ void k_tile_w_dgr(const float* __restrict__ W, uint16_t* __restrict__ Wt, int O, int I, int B, int RPT,
                              int nmt) {
   const int nkb = O / TC_KB;
   const int64_t per = 128 * TC_KB;
@@ -79,8 +92,8 @@ __global__ void k_tile_w_dgr(const float* __restrict__ W, uint16_t* __restrict__
   const int mt = (int)(blk / nkb), kb = (int)(blk - (int64_t)mt * nkb);
   const int e = r8 & 7, row = (r8 >> 3) & 127, ch = r8 >> 10;
   const int o = kb * TC_KB + 8 * ch + e;
-  const int il = row / B, n = row - il * B, i = mt * IPT + il;
-  const float w = (il < IPT && i < I) ? W[((int64_t)o * I + i) * B + n] : 0.f;
+  const int64_t kr = (int64_t)mt * RPT + row, K = (int64_t)I * B;
+  const float w = (row < RPT && kr < K) ? W[(int64_t)o * K + kr] : 0.f;
   uint16_t hi, lo;
   tc::split1_bf16(w, hi, lo);
   uint16_t* dst = Wt + blk * 2 * per;
@@ -91,7 +104,7 @@ __global__ void k_tile_w_dgr(const float* __restrict__ W, uint16_t* __restrict__
 template <int NF, int NS, int M, int OO>
 __global__ void __launch_bounds__(DgrCfg<NF, NS, M, OO>::THREADS, 1)
     k_dgrad_tc(const __grid_constant__ CUtensorMap tmX, const uint16_t* __restrict__ Ysplit,
-               const uint16_t* __restrict__ Wtiled, float* __restrict__ Xbar, int64_t P, int I, int IPT, int nmt,
+               const uint16_t* __restrict__ Wtiled, float* __restrict__ Xbar, int64_t P, int I, int RPT, int nmt,
                BasisCfg bc, int dbg) {
   using Cfg = DgrCfg<NF, NS, M, OO>;
   constexpr int C = Cfg::C, NP = Cfg::NP, N = Cfg::N, NKB = Cfg::NKB, NSTAGE = Cfg::NSTAGE;
@@ -103,6 +116,7 @@ __global__ void __launch_bounds__(DgrCfg<NF, NS, M, OO>::THREADS, 1)
   uint8_t* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);   // keeps the shared address space visible to the compiler (STS/LDS, not generic ST/LD)
   float* jets = reinterpret_cast<float*>(smem + NSTAGE * Cfg::STAGE_BYTES);   // [2][NP][C][IPTB] input jets
   float* S = jets + 2 * Cfg::JET_FLOATS;                      // epilogue slice [SLICE_P*C][DGR_SST]
+  float* carry = S + Cfg::S_FLOATS;                           // [2][NP][C] partial adjoints of split inputs
   __shared__ __align__(8) uint64_t full_bar[NSTAGE], empty_bar[NSTAGE], acc_full[2], acc_empty[2];
   __shared__ __align__(8) uint64_t jet_full[2], jet_empty[2];
   __shared__ uint32_t tmem_base_sh;
@@ -140,8 +154,10 @@ __global__ void __launch_bounds__(DgrCfg<NF, NS, M, OO>::THREADS, 1)
       tc::mbar_wait(&acc_full[buf], (uint32_t)((mt >> 1) & 1));
       tc::tc_fence_after();
       tc::mbar_wait(&jet_full[buf], (uint32_t)((mt >> 1) & 1));
-      const float* js = jets + buf * Cfg::JET_FLOATS + ((mt * IPT) & 3);   // [NP][C][IPTB] from input (mt*IPT) & ~3
-      const int n_in = min(IPT, I - mt * IPT);    // inputs in this tile
+      const int B = bc.B;
+      const int row0 = mt * RPT, nrows = min(RPT, I * B - row0);   // this tile's K rows
+      const int i_first = row0 / B, n_in = (row0 + nrows - 1) / B - i_first + 1;
+      const float* js = jets + buf * Cfg::JET_FLOATS + (i_first & 3);   // [NP][C][IPTB] from input i_first & ~3
 #pragma unroll 1
       for (int sl = 0; sl < NP / SLICE_P; ++sl) {
         const uint32_t tb = tmem + ((uint32_t)(qw * 32) << 16) + (uint32_t)(buf * N + sl * SLICE_P * C);
@@ -162,8 +178,9 @@ __global__ void __launch_bounds__(DgrCfg<NF, NS, M, OO>::THREADS, 1)
           const int il = task % n_in, pq = task / n_in;
           const int pl = sl * SLICE_P + pq;
           const int64_t p = p0 + pl;
-          const int i = mt * IPT + il;
+          const int i = i_first + il;
           if (p >= P) continue;
+          const int n_lo = max(0, row0 - i * B), n_hi = min(B, row0 + nrows - i * B);   // this tile's bases of i
           const float* jq = js + (pl * C) * DGR_IPTB + il;
           const float x = jq[0];
           float dx[NF > 0 ? NF : 1], ddx[NS > 0 ? NS : 1];
@@ -177,12 +194,12 @@ __global__ void __launch_bounds__(DgrCfg<NF, NS, M, OO>::THREADS, 1)
           for (int a = 0; a < NF; ++a) dxb[a] = 0.f;
 #pragma unroll
           for (int a = 0; a < NS; ++a) ddxb[a] = 0.f;
-          const float* Sp = S + (pq * C) * DGR_SST + il * bc.B;
+          const float* Sp = S + (pq * C) * DGR_SST + (i * B - row0);   // row of basis n: i*B + n - row0
 #pragma unroll
           for (int rr = 0; rr < KMAX; ++rr) {
             if (rr > bc.k) break;
             const int n = n0 + rr;
-            if (n < 0 || n >= bc.B) continue;
+            if (n < n_lo || n >= n_hi) continue;
             float v0, v1, v2, v3;
             hr_eval<M, (NS > 0 ? 3 : 2)>(basis_q(x, n, bc), bc.sc, v0, v1, v2, v3);
             float ab[C];
@@ -201,6 +218,24 @@ __global__ void __launch_bounds__(DgrCfg<NF, NS, M, OO>::THREADS, 1)
               dxb[a] = fmaf(2.f * g * v2, dx[a], dxb[a]);
               ddxb[a] = fmaf(g, v1, ddxb[a]);
             }
+          }
+          // carries alternate by tile parity: a tile reads its predecessor's and writes its own
+          if (n_lo > 0) {                          // input started in the previous tile: add its part
+            const float* cp = carry + (((mt + 1) & 1) * NP + pl) * C;
+            xb += cp[0];
+#pragma unroll
+            for (int a = 0; a < NF; ++a) dxb[a] += cp[1 + a];
+#pragma unroll
+            for (int a = 0; a < NS; ++a) ddxb[a] += cp[1 + NF + a];
+          }
+          float* cp = carry + ((mt & 1) * NP + pl) * C;
+          if (n_hi < B) {                          // input continues in the next tile: carry the part
+            cp[0] = xb;
+#pragma unroll
+            for (int a = 0; a < NF; ++a) cp[1 + a] = dxb[a];
+#pragma unroll
+            for (int a = 0; a < NS; ++a) cp[1 + NF + a] = ddxb[a];
+            continue;
           }
           float* out = Xbar + p * (int64_t)(C * I) + i;
           out[0] = xb;
@@ -275,7 +310,7 @@ __global__ void __launch_bounds__(DgrCfg<NF, NS, M, OO>::THREADS, 1)
         const int jb = mt & 1;
         if (mt >= 2) tc::mbar_wait(&jet_empty[jb], (uint32_t)(((mt >> 1) - 1) & 1));
         tc::mbar_arrive_expect_tx(&jet_full[jb], Cfg::JET_FLOATS * 4);
-        tc::tma_load_3d(jets + jb * Cfg::JET_FLOATS, &tmX, (mt * IPT) & ~3, 0, (int)p0, &jet_full[jb]);
+        tc::tma_load_3d(jets + jb * Cfg::JET_FLOATS, &tmX, ((mt * RPT) / bc.B) & ~3, 0, (int)p0, &jet_full[jb]);
       }
     }
     __syncwarp();

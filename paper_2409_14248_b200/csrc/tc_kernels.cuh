@@ -473,9 +473,9 @@ hrkan_status tc_refresh_weights(hrkan_net* net, cudaStream_t st) {
     HR_LAUNCH(HRKAN_K_OTHER, "k_tile_w_fwd",
               k_tile_w_fwd<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(net->params + net->w_off[l], ls.w_fwd, O, OP, K,
                                                                           ls.nkb));
-    // W^T tiles for the dgrad kernel (input-aligned M-tiles)
-    const int IPT = 128 / net->B;
-    ls.ntile_dgr = (I + IPT - 1) / IPT;
+    // W^T tiles for the dgrad kernel (contiguous 128-row M-tiles, or input-aligned for B < 11)
+    const int RPT = dgr_rows_per_tile(net->B, net->D);
+    ls.ntile_dgr = (int)((K + RPT - 1) / RPT);
     const size_t nd = (size_t)ls.ntile_dgr * (O / TC_KB) * 2 * 128 * TC_KB;
     if (!ls.w_dgr) {
       if (cudaMalloc(&ls.w_dgr, nd * sizeof(uint16_t)) != cudaSuccess) return fail(HRKAN_ENOMEM, "tc weight alloc");
@@ -483,7 +483,7 @@ hrkan_status tc_refresh_weights(hrkan_net* net, cudaStream_t st) {
     const int64_t totd = (int64_t)ls.ntile_dgr * (O / TC_KB) * 128 * TC_KB;
     HR_LAUNCH(HRKAN_K_OTHER, "k_tile_w_dgr",
               k_tile_w_dgr<<<(unsigned)((totd + 255) / 256), 256, 0, st>>>(net->params + net->w_off[l], ls.w_dgr, O, I,
-                                                                          net->B, IPT, ls.ntile_dgr));
+                                                                          net->B, RPT, ls.ntile_dgr));
   }
   return HRKAN_OK;
 }
@@ -636,7 +636,8 @@ hrkan_status launch_dgrad_tc(hrkan_net* net, int l, const float* X, const float*
   const unsigned grid = (unsigned)((n + Cfg::NP - 1) / Cfg::NP);
   HR_LAUNCH(HRKAN_K_DGRAD_HIDDEN, "k_dgrad_tc",
             kfn<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, st>>>(tmX, (const uint16_t*)net->tc_yd.p, ls.w_dgr, Xbar, n, I,
-                                                            128 / net->B, ls.ntile_dgr, net->bc, net->tc_dbg));
+                                                            dgr_rows_per_tile(net->B, net->D), ls.ntile_dgr, net->bc,
+                                                            net->tc_dbg));
   return HRKAN_OK;
 }
 
@@ -649,7 +650,7 @@ hrkan_status tc_dgrad_layer(hrkan_net* net, int l, const float* X, const float* 
     return HRKAN_OK;
   } else {
     if (!tc_layer_ok(net, l) || l >= (int)net->tc_layers.size() || !net->tc_layers[l].w_dgr) return HRKAN_OK;
-    if (128 / net->B + 3 > DGR_IPTB) return HRKAN_OK;   // input-aligned M-tile wider than the jet box
+    if (!dgr_tile_ok(net->B, net->D)) return HRKAN_OK;   // an M-tile's inputs would not fit the jet box
     const int O = net->widths[l + 1];
     if (O == 64) HR_TRY(launch_dgrad_tc<NF, NS, M, 64>(net, l, X, Ybar, Xbar, n, st));
     else if (O == 128) HR_TRY(launch_dgrad_tc<NF, NS, M, 128>(net, l, X, Ybar, Xbar, n, st));
