@@ -133,7 +133,7 @@ __global__ void __launch_bounds__(FwdCfg<NF, NS, M, OO>::THREADS, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < NSTAGE; ++s) {
-      tc::mbar_init(&full_bar[s], TC_GEN_THREADS + 1);
+      tc::mbar_init(&full_bar[s], (TC_GEN_THREADS / 32) * tc::ARRIVALS_PER_WARP + 1);   // one generator group + W producer
       tc::mbar_init(&empty_bar[s], 1);
     }
     for (int a = 0; a < NACC; ++a) {
@@ -284,8 +284,7 @@ __global__ void __launch_bounds__(FwdCfg<NF, NS, M, OO>::THREADS, 1)
           *reinterpret_cast<uint2*>(a_lo + aoff + row * 16) = ll;
         }
       }
-      tc::fence_proxy_async_smem();
-      tc::mbar_arrive(&full_bar[s]);
+      tc::warp_arrive_after_writes(&full_bar[s]);
       // advance to this group's next K-block
       n0 += dn; i0 += di;
       if (n0 >= B) { n0 -= B; ++i0; }

@@ -54,6 +54,25 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 #endif
 }
 
+// Producer-side arrival of a warp's generic-proxy smem writes: every lane fences its writes to the
+// async proxy, the warp converges, one lane arrives (HRKAN_WARP_ARRIVE) -- the barrier then counts
+// warps, not threads (32x fewer arrive operations on the stage barrier).  Without the switch every
+// thread arrives.
+#ifndef HRKAN_WARP_ARRIVE
+#define HRKAN_WARP_ARRIVE 0
+#endif
+constexpr unsigned ARRIVALS_PER_WARP = HRKAN_WARP_ARRIVE ? 1u : 32u;
+__device__ __forceinline__ void fence_proxy_async_smem();
+__device__ __forceinline__ void warp_arrive_after_writes(uint64_t* bar) {
+  fence_proxy_async_smem();
+#if HRKAN_WARP_ARRIVE
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) mbar_arrive(bar);
+#else
+  mbar_arrive(bar);
+#endif
+}
+
 // generic-proxy smem writes -> visible to the async proxy (tensor core / bulk copy)
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
