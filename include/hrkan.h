@@ -128,8 +128,9 @@ hrkan_status hrkan_adam_step(hrkan_net_t net, const float* grad, float lr, float
  * workspace, SURVEY §7 hard part (f)).  0 = default.  EINVAL: chunk < 0. */
 hrkan_status hrkan_set_chunk_points(hrkan_net_t net, int64_t chunk);
 
-/* Select the engine: 0 = auto (one-launch fused kernel for tiny nets -- every width <= 8, <= 4 layers
- * -- else tcgen05 tensor cores where a hidden layer is wide and SIMT FFMA elsewhere), 1 = force the
+/* Select the engine: 0 = auto (one-launch fused kernel for tiny nets -- every width <= 8, <= 4 layers,
+ * <= 2048 parameters, k <= 7; its last block reduces the gradient -- else tcgen05 tensor cores where a
+ * hidden layer is wide (O in {64,128,256}, I % 8 == 0, G+k >= 8) and SIMT FFMA elsewhere), 1 = force the
  * layered SIMT FFMA kernels, 2 = force tcgen05 where supported (layered).
  * EINVAL: unknown mode. */
 hrkan_status hrkan_set_engine(hrkan_net_t net, int32_t mode);
