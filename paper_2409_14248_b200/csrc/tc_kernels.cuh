@@ -31,6 +31,11 @@ constexpr int TC_GEN_THREADS = 128;   // one generator group (4 warps); the grou
 // Generator groups (all also drain the accumulators): 4 where the register budget of 19 warps allows
 // it without spills (measured: C4 forward 4.24 -> 3.78 ms, C3 1.83 -> 1.68 ms per 2^18 points), else 3
 // (C = 3 and C = 5 at O >= 128 spill with 4; C5's C = 7 layer was 2 % slower with 4).
+// forward generator arithmetic on packed fp32 pairs (two K slots per FFMA2/FMUL2) for m >= 3
+// (C4 forward 3.16 -> 2.75 ms, C3 1.42 -> 1.25 ms, C5 10.8 -> 10.5 ms per 2^18 points)
+#ifndef HRKAN_FWD_F32X2
+#define HRKAN_FWD_F32X2 1
+#endif
 #ifndef HRKAN_FWD_NGEN
 #define HRKAN_FWD_NGEN 0
 #endif
@@ -66,7 +71,7 @@ struct FwdCfg {
   static constexpr int STAGE_BYTES = W_STAGE_BYTES + A_STAGE_BYTES;
   static constexpr int CB = C | 1;                           // box channels (odd: conflict-free window reads)
   static constexpr int WIN_FLOATS = NP * CB * TC_WIN;        // TMA box [NP points][CB][TC_WIN inputs]
-  static constexpr int FIXED_BYTES = 4 * TC_NWIN * WIN_FLOATS + 4 * 256 + 1024;
+  static constexpr int FIXED_BYTES = 4 * TC_NWIN * WIN_FLOATS + 2 * 4 * 256 + 1024;   // windows, ctr, -ctr*sc
   static constexpr int NSTAGE_FIT = (225 * 1024 - FIXED_BYTES) / STAGE_BYTES;   // static smem + margin
   static constexpr int NSTAGE = NSTAGE_FIT > 6 ? 6 : NSTAGE_FIT;
   static constexpr int SMEM_BYTES = NSTAGE * STAGE_BYTES + FIXED_BYTES;
@@ -121,6 +126,7 @@ __global__ void __launch_bounds__(FwdCfg<NF, NS, M, OO>::THREADS, 1)
   uint8_t* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);   // keeps the shared address space visible to the compiler (STS/LDS, not generic ST/LD)
   float* win = reinterpret_cast<float*>(smem + NSTAGE * Cfg::STAGE_BYTES);   // [TC_NWIN][NP][C][TC_WIN]
   float* ctr = win + TC_NWIN * Cfg::WIN_FLOATS;              // basis centres mid_n, n < B
+  float* ncs = ctr + 256;                                     // -mid_n * sc (packed-pair generator)
   __shared__ __align__(8) uint64_t full_bar[NSTAGE], empty_bar[NSTAGE], acc_full[NACC], acc_empty[NACC];
   __shared__ __align__(8) uint64_t win_full[TC_NWIN], win_empty[TC_NWIN];
   __shared__ uint32_t tmem_base_sh;
@@ -146,7 +152,10 @@ __global__ void __launch_bounds__(FwdCfg<NF, NS, M, OO>::THREADS, 1)
     }
     tc::fence_mbar_init();
   }
-  for (int n = threadIdx.x; n < bc.B; n += blockDim.x) ctr[n] = fmaf((float)n, bc.h, bc.mid0);
+  for (int n = threadIdx.x; n < bc.B; n += blockDim.x) {
+    ctr[n] = fmaf((float)n, bc.h, bc.mid0);
+    ncs[n] = -ctr[n] * bc.sc;
+  }
   if (warp == TC_MMA_WARP) tc::tmem_alloc<Cfg::TMEM_COLS>(&tmem_base_sh);
   tc::tc_fence_before();
   __syncthreads();
@@ -256,6 +265,46 @@ __global__ void __launch_bounds__(FwdCfg<NF, NS, M, OO>::THREADS, 1)
           for (int a = 0; a < NS; ++a) jddx[h][a] = wp[(1 + NF + a) * TC_WIN];
         }
         float va[C][4];
+#if HRKAN_FWD_F32X2
+        if constexpr (M >= 3) {
+          // two K slots per instruction (FFMA2/FMUL2); same formulas as hr_eval with t clamped at 0
+          // (NaN kept), so every derivative vanishes outside the support (m >= 3)
+          const uint64_t SC2 = tc::pk2(bc.sc, bc.sc), ONE2 = tc::pk2(1.f, 1.f), NEG2 = tc::pk2(-1.f, -1.f);
+          const float c1 = -2.f * M * bc.sc, c2 = -2.f * M * bc.sc * bc.sc, k2 = -(2.f * M - 1.f);
+          const uint64_t C12 = tc::pk2(c1, c1), C22 = tc::pk2(c2, c2), K22 = tc::pk2(k2, k2);
+#pragma unroll
+          for (int e = 0; e < 4; e += 2) {
+            const int na = n0 + e, nb = n0 + e + 1;
+            const bool ha = na >= B, hb = nb >= B;
+            const int nna = ha ? na - B : na, nnb = hb ? nb - B : nb;
+            const uint64_t qq = tc::fma2(tc::pk2(ha ? jx[1] : jx[0], hb ? jx[1] : jx[0]), SC2, tc::pk2(ncs[nna], ncs[nnb]));
+            const uint64_t q2 = tc::mul2(qq, qq);
+            float t0, t1;
+            tc::upk2(tc::fma2(q2, NEG2, ONE2), t0, t1);
+            t0 = (i0 * B + na < K) ? tc::max_nan(t0, 0.f) : 0.f;
+            t1 = (i0 * B + nb < K) ? tc::max_nan(t1, 0.f) : 0.f;
+            const uint64_t t = tc::pk2(t0, t1);
+            uint64_t tm2 = ONE2;
+#pragma unroll
+            for (int k = 0; k < M - 2; ++k) tm2 = tc::mul2(tm2, t);
+            const uint64_t tm1 = tc::mul2(tm2, t);
+            tc::upk2(tc::mul2(tm1, t), va[0][e], va[0][e + 1]);
+            const uint64_t v1 = tc::mul2(tc::mul2(qq, tm1), C12);
+            const uint64_t v2 = tc::mul2(tc::mul2(tm2, tc::fma2(q2, K22, ONE2)), C22);
+#pragma unroll
+            for (int a = 0; a < NF; ++a) {
+              const uint64_t d = tc::pk2(ha ? jdx[1][a] : jdx[0][a], hb ? jdx[1][a] : jdx[0][a]);
+              tc::upk2(tc::mul2(v1, d), va[1 + a][e], va[1 + a][e + 1]);
+            }
+#pragma unroll
+            for (int a = 0; a < NS; ++a) {
+              const uint64_t d = tc::pk2(ha ? jdx[1][a] : jdx[0][a], hb ? jdx[1][a] : jdx[0][a]);
+              const uint64_t dd = tc::pk2(ha ? jddx[1][a] : jddx[0][a], hb ? jddx[1][a] : jddx[0][a]);
+              tc::upk2(tc::fma2(tc::mul2(v2, d), d, tc::mul2(v1, dd)), va[1 + NF + a][e], va[1 + NF + a][e + 1]);
+            }
+          }
+        } else {
+#endif
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const int n = n0 + e;
@@ -275,6 +324,9 @@ __global__ void __launch_bounds__(FwdCfg<NF, NS, M, OO>::THREADS, 1)
             va[1 + NF + a][e] = fmaf(v2 * d1, d1, v1 * d2);
           }
         }
+#if HRKAN_FWD_F32X2
+        }
+#endif
 #pragma unroll
         for (int c = 0; c < C; ++c) {
           uint2 hh, ll;
