@@ -22,6 +22,11 @@ namespace {
 // (measured per 2^18 points: C4's C = 4 layers with 32-point slices and 12 warps 3.58 -> 2.65 ms, C3's
 // C = 5 layers with 24-point slices 1.29 -> 1.08 ms; C5's 7-channel slices stay at 16 points, 32 would
 // leave room for only 3 stages and was 30 % slower).
+// dgrad epilogue arithmetic on packed fp32 pairs (two bases per FFMA2/FMUL2) for m >= 4
+// (C4 dgrad 2.76 -> 2.55 ms, C3 1.12 -> 0.96 ms per 2^18 points)
+#ifndef HRKAN_DGR_F32X2
+#define HRKAN_DGR_F32X2 1
+#endif
 #ifndef HRKAN_DGR_SLICE_P
 #define HRKAN_DGR_SLICE_P 0
 #endif
@@ -195,6 +200,69 @@ __global__ void __launch_bounds__(DgrCfg<NF, NS, M, OO>::THREADS, 1)
 #pragma unroll
           for (int a = 0; a < NS; ++a) ddxb[a] = 0.f;
           const float* Sp = S + (pq * C) * DGR_SST + (i * B - row0);   // row of basis n: i*B + n - row0
+#if HRKAN_DGR_F32X2
+          if constexpr (M >= 4) {
+            // two bases per instruction (FFMA2/FMUL2); t clamped at 0 (NaN kept) zeroes v1..v3 outside
+            // the support and for bases outside this tile (m >= 4); their smem rows are clamped in range
+            const uint64_t ONE2 = tc::pk2(1.f, 1.f), NEG2 = tc::pk2(-1.f, -1.f);
+            const float sc = bc.sc, k2 = -(2.f * M - 1.f);
+            const uint64_t C12 = tc::pk2(-2.f * M * sc, -2.f * M * sc);
+            const uint64_t C22 = tc::pk2(-2.f * M * sc * sc, -2.f * M * sc * sc);
+            const uint64_t C32 = tc::pk2(4.f * M * (M - 1) * sc * sc * sc, 4.f * M * (M - 1) * sc * sc * sc);
+            const uint64_t K22 = tc::pk2(k2, k2), THREE2 = tc::pk2(3.f, 3.f), TWO2 = tc::pk2(2.f, 2.f);
+            uint64_t xb2 = tc::pk2(0.f, 0.f), dxb2[NF > 0 ? NF : 1], ddxb2[NS > 0 ? NS : 1], dx2[NF > 0 ? NF : 1],
+                     ddx2[NS > 0 ? NS : 1];
+#pragma unroll
+            for (int a = 0; a < NF; ++a) { dxb2[a] = xb2; dx2[a] = tc::pk2(dx[a], dx[a]); }
+#pragma unroll
+            for (int a = 0; a < NS; ++a) { ddxb2[a] = xb2; ddx2[a] = tc::pk2(ddx[a], ddx[a]); }
+#pragma unroll
+            for (int rr = 0; rr < KMAX; rr += 2) {
+              if (rr > bc.k) break;
+              const int na = n0 + rr, nb = n0 + rr + 1;
+              const bool oka = na >= n_lo && na < n_hi, okb = rr + 1 <= bc.k && nb >= n_lo && nb < n_hi;
+              const int ca = oka ? na : n_lo, cb = okb ? nb : n_lo;          // in-tile rows for the loads
+              const uint64_t qq = tc::pk2(basis_q(x, na, bc), basis_q(x, nb, bc));
+              const uint64_t q2 = tc::mul2(qq, qq);
+              float t0, t1;
+              tc::upk2(tc::fma2(q2, NEG2, ONE2), t0, t1);
+              t0 = oka ? tc::max_nan(t0, 0.f) : 0.f;
+              t1 = okb ? tc::max_nan(t1, 0.f) : 0.f;
+              const uint64_t t = tc::pk2(t0, t1);
+              uint64_t tm3 = ONE2;
+#pragma unroll
+              for (int e = 0; e < M - 3; ++e) tm3 = tc::mul2(tm3, t);
+              const uint64_t tm2 = tc::mul2(tm3, t), tm1 = tc::mul2(tm2, t);
+              const uint64_t v1 = tc::mul2(tc::mul2(qq, tm1), C12);
+              const uint64_t kq = tc::fma2(q2, K22, ONE2);                      // 1 - (2m-1) q^2
+              const uint64_t v2 = tc::mul2(tc::mul2(tm2, kq), C22);
+              const uint64_t v3 = tc::mul2(tc::mul2(tc::mul2(qq, tm3), tc::fma2(q2, K22, THREE2)), C32);
+              uint64_t ab[C];
+#pragma unroll
+              for (int c = 0; c < C; ++c) ab[c] = tc::pk2(Sp[c * DGR_SST + ca], Sp[c * DGR_SST + cb]);
+              xb2 = tc::fma2(ab[0], v1, xb2);
+#pragma unroll
+              for (int a = 0; a < NF; ++a) {
+                xb2 = tc::fma2(tc::mul2(ab[1 + a], v2), dx2[a], xb2);
+                dxb2[a] = tc::fma2(ab[1 + a], v1, dxb2[a]);
+              }
+#pragma unroll
+              for (int a = 0; a < NS; ++a) {
+                const uint64_t g = ab[1 + NF + a];
+                xb2 = tc::fma2(g, tc::fma2(tc::mul2(v3, dx2[a]), dx2[a], tc::mul2(v2, ddx2[a])), xb2);
+                dxb2[a] = tc::fma2(tc::mul2(TWO2, tc::mul2(g, v2)), dx2[a], dxb2[a]);
+                ddxb2[a] = tc::fma2(g, v1, ddxb2[a]);
+              }
+            }
+            float lo_, hi_;
+            tc::upk2(xb2, lo_, hi_);
+            xb = lo_ + hi_;
+#pragma unroll
+            for (int a = 0; a < NF; ++a) { tc::upk2(dxb2[a], lo_, hi_); dxb[a] = lo_ + hi_; }
+#pragma unroll
+            for (int a = 0; a < NS; ++a) { tc::upk2(ddxb2[a], lo_, hi_); ddxb[a] = lo_ + hi_; }
+          } else {
+#endif
 #pragma unroll
           for (int rr = 0; rr < KMAX; ++rr) {
             if (rr > bc.k) break;
@@ -219,6 +287,9 @@ __global__ void __launch_bounds__(DgrCfg<NF, NS, M, OO>::THREADS, 1)
               ddxb[a] = fmaf(g, v1, ddxb[a]);
             }
           }
+#if HRKAN_DGR_F32X2
+          }
+#endif
           // carries alternate by tile parity: a tile reads its predecessor's and writes its own
           if (n_lo > 0) {                          // input started in the previous tile: add its part
             const float* cp = carry + (((mt + 1) & 1) * NP + pl) * C;
