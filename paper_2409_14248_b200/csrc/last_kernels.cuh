@@ -20,11 +20,41 @@
 // (+ db, sum r^2, non-finite count), and k_reduce_last sums the blocks in a fixed order: the
 // result is bitwise reproducible for a fixed grid.
 #pragma once
+#include "tc_ptx.cuh"   // packed fp32 pair helpers (FFMA2 / FMUL2)
 
 namespace {   // internal linkage: every translation unit owns its kernels
 using namespace hrkan;
 
 constexpr int LF_WARPS = 4;
+
+// Output-layer basis arithmetic on packed fp32 pairs (two bases per FFMA2/FMUL2, m >= 4): v0..v3 of
+// bases na, nb at x with t = 1 - q^2 clamped at 0 (NaN kept), zero where !ok (outside [0, B)).
+#ifndef HRKAN_LAST_F32X2
+#define HRKAN_LAST_F32X2 1
+#endif
+template <int M>
+__device__ __forceinline__ void hr_eval_pair(float x, int na, int nb, bool oka, bool okb, const BasisCfg& bc,
+                                             uint64_t& v0, uint64_t& v1, uint64_t& v2, uint64_t& v3) {
+  using namespace tc;
+  const float sc = bc.sc, k2 = -(2.f * M - 1.f);
+  const uint64_t ONE2 = pk2(1.f, 1.f), NEG2 = pk2(-1.f, -1.f), K22 = pk2(k2, k2);
+  const uint64_t qq = pk2(basis_q(x, na, bc), basis_q(x, nb, bc));
+  const uint64_t q2 = mul2(qq, qq);
+  float t0, t1;
+  upk2(fma2(q2, NEG2, ONE2), t0, t1);
+  t0 = oka ? max_nan(t0, 0.f) : 0.f;
+  t1 = okb ? max_nan(t1, 0.f) : 0.f;
+  const uint64_t t = pk2(t0, t1);
+  uint64_t tm3 = ONE2;
+#pragma unroll
+  for (int e = 0; e < M - 3; ++e) tm3 = mul2(tm3, t);
+  const uint64_t tm2 = mul2(tm3, t), tm1 = mul2(tm2, t);
+  v0 = mul2(tm1, t);
+  const float c1 = -2.f * M * sc, c2 = c1 * sc, c3 = 4.f * M * (M - 1) * sc * sc * sc;
+  v1 = mul2(mul2(qq, tm1), pk2(c1, c1));
+  v2 = mul2(mul2(tm2, fma2(q2, K22, ONE2)), pk2(c2, c2));
+  v3 = mul2(mul2(mul2(qq, tm3), fma2(q2, K22, pk2(3.f, 3.f))), pk2(c3, c3));
+}
 enum LastMode { LAST_JET = 0, LAST_POISSON = 1, LAST_BURGERS = 2, LAST_BOUNDARY = 3 };
 
 template <int NF, int NS, int M, int MODE, bool FIRST>
@@ -60,6 +90,25 @@ __global__ void __launch_bounds__(32 * LF_WARPS)
       if (x != x) s[0] += x;            // propagate NaN inputs into the residual / flag
       const int n0 = first_basis(x, bc);
       float T0 = 0.f, T1 = 0.f, T2 = 0.f;
+      if constexpr (HRKAN_LAST_F32X2 && M >= 4) {
+        uint64_t P0 = tc::pk2(0.f, 0.f), P1 = P0, P2 = P0;
+#pragma unroll
+        for (int r = 0; r < KMAX; r += 2) {
+          if (r > bc.k) break;
+          const int na = n0 + r, nb = na + 1;
+          const bool oka = na >= 0 && na < B, okb = r + 1 <= bc.k && nb >= 0 && nb < B;
+          uint64_t v0, v1, v2, v3;
+          hr_eval_pair<M>(x, na, nb, oka, okb, bc, v0, v1, v2, v3);
+          const uint64_t w = tc::pk2(oka ? __ldg(W + i * B + na) : 0.f, okb ? __ldg(W + i * B + nb) : 0.f);
+          P0 = tc::fma2(w, v0, P0);
+          P1 = tc::fma2(w, v1, P1);
+          P2 = tc::fma2(w, v2, P2);
+        }
+        float lo_, hi_;
+        tc::upk2(P0, lo_, hi_); T0 = lo_ + hi_;
+        tc::upk2(P1, lo_, hi_); T1 = lo_ + hi_;
+        tc::upk2(P2, lo_, hi_); T2 = lo_ + hi_;
+      } else {
 #pragma unroll
       for (int r = 0; r < KMAX; ++r) {
         if (r > bc.k) break;
@@ -71,6 +120,7 @@ __global__ void __launch_bounds__(32 * LF_WARPS)
         T0 = fmaf(w, v0, T0);
         T1 = fmaf(w, v1, T1);
         T2 = fmaf(w, v2, T2);
+      }
       }
       s[0] += T0;
 #pragma unroll
@@ -238,6 +288,7 @@ __global__ void __launch_bounds__(RL_COLS * RL_CHAINS)
 // ---------------------------------------------------------------------------------------------
 constexpr int LV_PB = 4;
 
+
 // Transposing warp sum of NV values per lane (NV a power of two <= 32): at each step of width h the
 // lanes with bit h set keep the upper half of their values and send the lower half (and vice versa),
 // so NV - 1 shuffles replace 5*NV; the remaining butterflies (h >= NV) finish the sum.  Afterwards
@@ -325,6 +376,25 @@ __global__ void __launch_bounds__(256, 3)
       if (x != x) s[0] = x;
       const int n0 = first_basis(x, bc);
       float T0 = 0.f, T1 = 0.f, T2 = 0.f;
+      if constexpr (HRKAN_LAST_F32X2 && M >= 4) {
+        uint64_t P0 = tc::pk2(0.f, 0.f), P1 = P0, P2 = P0;
+#pragma unroll
+        for (int r = 0; r < KMAX; r += 2) {
+          if (r > bc.k) break;
+          const int na = n0 + r, nb = na + 1;
+          const bool oka = na >= 0 && na < B, okb = r + 1 <= bc.k && nb >= 0 && nb < B;
+          uint64_t v0, v1, v2, v3;
+          hr_eval_pair<M>(x, na, nb, oka, okb, bc, v0, v1, v2, v3);
+          const uint64_t w = tc::pk2(oka ? __ldg(W + i * B + na) : 0.f, okb ? __ldg(W + i * B + nb) : 0.f);
+          P0 = tc::fma2(w, v0, P0);
+          P1 = tc::fma2(w, v1, P1);
+          P2 = tc::fma2(w, v2, P2);
+        }
+        float lo_, hi_;
+        tc::upk2(P0, lo_, hi_); T0 = lo_ + hi_;
+        tc::upk2(P1, lo_, hi_); T1 = lo_ + hi_;
+        tc::upk2(P2, lo_, hi_); T2 = lo_ + hi_;
+      } else {
 #pragma unroll
       for (int r = 0; r < KMAX; ++r) {
         if (r > bc.k) break;
@@ -336,6 +406,7 @@ __global__ void __launch_bounds__(256, 3)
         T0 = fmaf(w, v0, T0);
         T1 = fmaf(w, v1, T1);
         T2 = fmaf(w, v2, T2);
+      }
       }
       s[0] += T0;
 #pragma unroll
@@ -438,6 +509,30 @@ __global__ void __launch_bounds__(256, 3)
       }
       const int n0 = first_basis(x, bc);
       float T1 = 0.f, T2 = 0.f, T3 = 0.f;
+      if constexpr (HRKAN_LAST_F32X2 && M >= 4) {
+        const uint64_t Y0 = tc::pk2(y[0], y[0]), G1 = tc::pk2(g1, g1), G2 = tc::pk2(g2, g2);
+        uint64_t P1 = tc::pk2(0.f, 0.f), P2 = P1, P3 = P1;
+#pragma unroll
+        for (int rr = 0; rr < KMAX; rr += 2) {
+          if (rr > bc.k) break;
+          const int na = n0 + rr, nb = na + 1;
+          const bool oka = na >= 0 && na < B, okb = rr + 1 <= bc.k && nb >= 0 && nb < B;
+          uint64_t v0, v1, v2, v3;
+          hr_eval_pair<M>(x, na, nb, oka, okb, bc, v0, v1, v2, v3);
+          float ca, cb;
+          tc::upk2(tc::fma2(Y0, v0, tc::fma2(G1, v1, tc::mul2(G2, v2))), ca, cb);
+          if (oka) acc[na * I + i] += ca;
+          if (okb) acc[nb * I + i] += cb;
+          const uint64_t w = tc::pk2(oka ? __ldg(W + i * B + na) : 0.f, okb ? __ldg(W + i * B + nb) : 0.f);
+          P1 = tc::fma2(w, v1, P1);
+          P2 = tc::fma2(w, v2, P2);
+          P3 = tc::fma2(w, v3, P3);
+        }
+        float lo_, hi_;
+        tc::upk2(P1, lo_, hi_); T1 = lo_ + hi_;
+        tc::upk2(P2, lo_, hi_); T2 = lo_ + hi_;
+        tc::upk2(P3, lo_, hi_); T3 = lo_ + hi_;
+      } else {
 #pragma unroll
       for (int rr = 0; rr < KMAX; ++rr) {
         if (rr > bc.k) break;
@@ -450,6 +545,7 @@ __global__ void __launch_bounds__(256, 3)
         T1 = fmaf(w, v1, T1);
         T2 = fmaf(w, v2, T2);
         T3 = fmaf(w, v3, T3);
+      }
       }
       float* out = Xbar + p * (int64_t)(C * I) + i;
       out[0] = fmaf(y[0], T1, fmaf(g1, T2, g2 * T3));
