@@ -17,9 +17,10 @@ constexpr int FL_THREADS = 256;
 
 // Shared basis table entry for (point, coordinate a): first basis n0 and v, v', v'' of the k+1
 // candidates n0 .. n0+k (zero where n is outside [0, B) or x outside the support).
-struct FlBasis {
+struct __align__(8) FlBasis {
+  float v[3][KMAX];     // 8-byte aligned pairs v[c][2j], v[c][2j+1] (packed-pair loads)
   int n0;
-  float v[3][KMAX];
+  int pad;
 };
 
 template <int D, int M, int ND>
@@ -100,17 +101,23 @@ __global__ void __launch_bounds__(FL_THREADS) k_fwd_first(const float* __restric
         for (int c = 1; c < C; ++c) acc[c] = 0.f;
         for (int a = 0; a < Dr; ++a) {
           const FlBasis& t = tab[q * Dr + a];
-          float s0 = 0.f, s1 = 0.f, s2 = 0.f;
+          // two bases per FFMA2 (table pairs are 8-byte aligned)
+          uint64_t S0 = tc::pk2(0.f, 0.f), S1 = S0, S2 = S0;
 #pragma unroll
-          for (int r = 0; r < KMAX; ++r) {
+          for (int r = 0; r < KMAX; r += 2) {
             if (r > bc.k) break;
-            const int n = t.n0 + r;
-            if (n < 0 || n >= bc.B) continue;
-            const float w = __ldg(Wt + ((int64_t)a * bc.B + n) * O + o);
-            s0 = fmaf(w, t.v[0][r], s0);
-            s1 = fmaf(w, t.v[1][r], s1);
-            s2 = fmaf(w, t.v[2][r], s2);
+            const int na = t.n0 + r, nb = na + 1;
+            const bool oka = na >= 0 && na < bc.B, okb = r + 1 <= bc.k && nb >= 0 && nb < bc.B;
+            const uint64_t w = tc::pk2(oka ? __ldg(Wt + ((int64_t)a * bc.B + na) * O + o) : 0.f,
+                                       okb ? __ldg(Wt + ((int64_t)a * bc.B + nb) * O + o) : 0.f);
+            S0 = tc::fma2(w, *reinterpret_cast<const uint64_t*>(&t.v[0][r]), S0);
+            S1 = tc::fma2(w, *reinterpret_cast<const uint64_t*>(&t.v[1][r]), S1);
+            S2 = tc::fma2(w, *reinterpret_cast<const uint64_t*>(&t.v[2][r]), S2);
           }
+          float s0, s1, s2, hi_;
+          tc::upk2(S0, s0, hi_); s0 += hi_;
+          tc::upk2(S1, s1, hi_); s1 += hi_;
+          tc::upk2(S2, s2, hi_); s2 += hi_;
           acc[0] += s0;
 #pragma unroll
           for (int aa = 0; aa < NF; ++aa)
@@ -205,12 +212,20 @@ __global__ void __launch_bounds__(FL_THREADS) k_wgrad_first(const float* __restr
 #pragma unroll
           for (int aa = 0; aa < NS; ++aa)
             if (aa == a) y2 = y[1 + NF + aa];
+          // two bases per FFMA2/FMUL2 (table pairs are 8-byte aligned); the accumulations stay per basis
+          const uint64_t Y0 = tc::pk2(y[0], y[0]), Y1 = tc::pk2(y1, y1), Y2 = tc::pk2(y2, y2);
 #pragma unroll
-          for (int r = 0; r < KMAX; ++r) {
+          for (int r = 0; r < KMAX; r += 2) {
             if (r > bc.k) break;
-            const int n = t.n0 + r;
-            if (n < 0 || n >= B) continue;
-            accq[(a * B + n) * O + o] += fmaf(y[0], t.v[0][r], fmaf(y1, t.v[1][r], y2 * t.v[2][r]));
+            const int na = t.n0 + r, nb = na + 1;
+            const bool oka = na >= 0 && na < B, okb = r + 1 <= bc.k && nb >= 0 && nb < B;
+            const uint64_t c2 = tc::fma2(Y0, *reinterpret_cast<const uint64_t*>(&t.v[0][r]),
+                                         tc::fma2(Y1, *reinterpret_cast<const uint64_t*>(&t.v[1][r]),
+                                                  tc::mul2(Y2, *reinterpret_cast<const uint64_t*>(&t.v[2][r]))));
+            float ca, cb;
+            tc::upk2(c2, ca, cb);
+            if (oka) accq[(a * B + na) * O + o] += ca;
+            if (okb) accq[(a * B + nb) * O + o] += cb;
           }
         }
       }
