@@ -3,22 +3,22 @@
 // The hidden KAN layer is the dense contraction of PAPER.md:45/:87 ("KAN layer as a matrix
 // operation") applied to every jet channel:
 //     Y[(p,c), o] = sum_{K=(i,n)} A^c[p, K] W[o, K]      (+ b_o on the value channel c = 0)
-// with A^c generated on the fly from the saved input jet.  It runs as 3xTF32
-// on the 5th-generation tensor cores: W and A are split into tf32 hi/lo parts and
-//     D += W_hi A_hi + W_hi A_lo + W_lo A_hi
+// with A^c generated on the fly from the saved input jet.  It runs as bf16x3 on
+// the 5th-generation tensor cores: W and A are split into bf16 hi/lo parts and
+//     D += W_lo A_hi + W_hi A_lo + W_hi A_hi
 // accumulate in fp32 TMEM, which meets the north-star tolerance.
 //
 // Forward kernel k_fwd_tc (orientation "W rows x (point,channel) columns"):
-//   MMA M = output neurons o (128-row tiles; O = 128 or 256 -> 1 or 2 tiles, both share the B tile),
-//   MMA N = NP points x C channels of one point tile (channel-major columns n = c*NP + p),
-//   MMA K = I*B (dense over all bases, zero-padded to a multiple of KB).
-//   smem stage = { W_hi, W_lo tiles [KB/4 chunks][O rows][4] via one 1-D bulk copy of a
-//                  pre-tiled global copy;  A_hi, A_lo tiles [KB/4][N][4] written by the generator
+//   MMA M = output neurons o (128-row tiles; O = 64/128 -> 1 zero-padded or full tile, 256 -> 2 tiles
+//   sharing the B tile), MMA N = NP points x C channels of one point tile (channel-major columns
+//   n = c*NP + p), MMA K = I*B (dense over all bases, zero-padded to a multiple of KB).
+//   smem stage = { W_hi, W_lo tiles [2 chunks][OP rows][8] bf16 via one 1-D bulk copy of a pre-tiled
+//                  global copy;  A_hi, A_lo tiles [2 chunks][N rows][8] written by the generator
 //                  warps }, NSTAGE-deep mbarrier ring.  The generators read the saved input jet from
-//   a ring of TMA-loaded windows X[tile points][C][8 inputs] (coalesced, prefetched ahead).
-//   warps 0-7: two generator groups (alternate K-blocks), then the segment drains (TMEM -> +bias ->
-//   Y[p][c][o], coalesced); warp 8: TMEM allocator + single-thread MMA issuer; warp 9: W bulk copies;
-//   warp 10: jet-window TMA loads.
+//   a ring of TMA-loaded windows X[tile points][C|1][4 inputs] (coalesced, prefetched ahead).
+//   warps 0 .. 4*NGEN-1: NGEN generator groups (K-blocks kb = grp mod NGEN), which also drain the
+//   TMEM segments (+bias -> Y[p][c][o], coalesced); then the MMA warp (TMEM allocator + single-thread
+//   tcgen05.mma issuer), the W bulk-copy warp and the jet-window TMA warp (FwdCfg::*_WARP).
 #pragma once
 #include "tc_ptx.cuh"
 
@@ -26,7 +26,7 @@ namespace {
 
 using namespace hrkan;
 
-constexpr int TC_KB = 16;          // K per pipeline stage (two tf32 MMA K-steps of 8)
+constexpr int TC_KB = 16;          // K per pipeline stage (one bf16 MMA K-step)
 constexpr int TC_GEN_THREADS = 128;   // one generator group (4 warps); the group handles every other K-block
 // Generator groups (all also drain the accumulators): 4 where the register budget of 19 warps allows
 // it without spills (measured: C4 forward 4.24 -> 3.78 ms, C3 1.83 -> 1.68 ms per 2^18 points), else 3
@@ -107,12 +107,12 @@ __global__ void k_tile_w_fwd(const float* __restrict__ W, uint16_t* __restrict__
   dst[per_kb + r] = lo;
 }
 
-// Forward hidden layer.  Warp roles:
-//   warps 0..7   two generator groups (K-blocks kb = grp mod 2), then the segment drains;
-//   warp 8       TMEM allocator + single-thread tcgen05.mma issuer;
-//   warp 9       1-D bulk copies of the pre-tiled W_hi/W_lo stage;
-//   warp 10      TMA loads of jet windows: X[p0 .. p0+NP)[C][8w .. 8w+8) -> smem ring (TC_NWIN deep),
-//                so the generators read the jets from shared memory (coalesced, latency hidden).
+// Forward hidden layer.  Warp roles (FwdCfg: NGEN = 3 or 4 generator groups of 4 warps):
+//   warps 0 .. 4*NGEN-1   generator groups (K-blocks kb = grp mod NGEN), then the segment drains;
+//   MMA_WARP              TMEM allocator + single-thread tcgen05.mma issuer;
+//   PROD_WARP             1-D bulk copies of the pre-tiled W_hi/W_lo stage;
+//   WIN_WARP              TMA loads of jet windows X[p0 .. p0+NP)[C|1][4w .. 4w+4) -> smem ring
+//                         (TC_NWIN deep), so the generators read the jets from shared memory.
 template <int NF, int NS, int M, int OO>
 __global__ void __launch_bounds__(FwdCfg<NF, NS, M, OO>::THREADS, 1)
     k_fwd_tc(const __grid_constant__ CUtensorMap tmX, const uint16_t* __restrict__ Wtiled, const float* __restrict__ bias,

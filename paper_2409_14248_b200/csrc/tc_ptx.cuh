@@ -1,6 +1,7 @@
 // tc_ptx.cuh -- thin inline-PTX wrappers for the sm_100a tensor-core path: mbarriers, the 1-D
-// bulk async copy (UBLKCP), TMEM allocation, tcgen05.mma (kind::tf32, cta_group::1),
-// tcgen05.commit and tcgen05.ld.  Descriptor bit layouts follow the sm_100 UMMA formats
+// bulk async copy (UBLKCP) and L2 prefetch, 3-D TMA loads, TMEM allocation, tcgen05.mma (kind::f16
+// with BF16 operands and F32 accumulate, cta_group::1), tcgen05.commit / ld / st, bf16 hi/lo splits
+// and packed fp32 pair arithmetic (FFMA2 / FMUL2).  Descriptor bit layouts follow the sm_100 UMMA formats
 // (shared-memory matrix descriptor and 32-bit instruction descriptor).
 #pragma once
 #include <cstdint>
@@ -161,24 +162,8 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo, uint
   return d;                 // base_offset 0, lbo_mode 0, layout SWIZZLE_NONE
 }
 
-// Instruction descriptor kind::tf32, D = f32, A/B = tf32; a_mn/b_mn = 1 for MN-major operands.
-__host__ __device__ constexpr uint32_t idesc_tf32(uint32_t M, uint32_t N, uint32_t a_mn = 0, uint32_t b_mn = 0) {
-  return (1u << 4)            // c_format F32
-         | (2u << 7)          // a_format TF32
-         | (2u << 10)         // b_format TF32
-         | (a_mn << 15) | (b_mn << 16) | ((N >> 3) << 17) | ((M >> 4) << 24);
-}
 
 // D[tmem] (+)= A[smem] * B[smem]^T   (single elected thread)
-__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                         uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
 
 // Instruction descriptor kind::f16 with BF16 A/B (K-major) and an F32 accumulator.
 __host__ __device__ constexpr uint32_t idesc_bf16(uint32_t M, uint32_t N) {
@@ -245,63 +230,6 @@ __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.
 // named barrier among `nthreads` threads (id 1..15; 0 is __syncthreads)
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
-}
-
-// 3xTF32 split: hi keeps the 19 tf32 bits (truncation), lo = x - hi exactly; the tensor core
-// reads lo's top 19 bits, so a*b ~ ah*bh + ah*bl + al*bh to ~2^-20 relative.
-__device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
-  hi = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
-  lo = x - hi;
-}
-
-// ------------------------------------------------------------------ CTA pairs (cta_group::2)
-__device__ __forceinline__ uint32_t cluster_ctarank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-// all threads of all CTAs of the cluster
-__device__ __forceinline__ void cluster_sync() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-// shared::cluster address of the same smem variable in CTA `rank` of the cluster
-__device__ __forceinline__ uint32_t mapa_u32(uint32_t saddr, uint32_t rank) {
-  uint32_t r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
-  return r;
-}
-// arrive (release at cluster scope) on an mbarrier given by its shared::cluster address
-__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
-}
-template <uint32_t NCOLS>
-__device__ __forceinline__ void tmem_alloc2(uint32_t* dst_smem) {   // whole warp, in each CTA of the pair
-  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
-               "n"(NCOLS)
-               : "memory");
-  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
-}
-template <uint32_t NCOLS>
-__device__ __forceinline__ void tmem_dealloc2(uint32_t taddr) {      // whole warp, in each CTA of the pair
-  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(NCOLS) : "memory");
-}
-// pair MMA (issued by the leader CTA only): D[256 rows over the 2 CTAs' TMEM] (+)= A[smem of both] B[smem of both]^T
-__device__ __forceinline__ void mma2_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                          uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
-// arrive on the mbarrier at the same smem offset in every CTA of `mask` when the leader's MMAs complete
-__device__ __forceinline__ void mma_commit2(uint64_t* bar, uint16_t mask) {
-  asm volatile(
-      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
-          smem_u32(bar)),
-      "h"(mask)
-      : "memory");
 }
 
 // bf16x3 split: x = hi + lo + r with hi = bf16_rn(x), lo = bf16_rn(x - hi),
