@@ -387,3 +387,28 @@ def test_paper_burgers_training_converges(torch_mod):
     r = mod.run(0, 3000, 1e-2, dev)
     assert r["train_loss"] < 0.1 * r0["train_loss"]
     assert r["train_loss"] < 1e-3
+
+
+@pytest.mark.parametrize("key", ["C3", "C4", "C5"])
+def test_nonfinite_inputs_flagged_tensor_core_path(torch_mod, key):
+    """Non-finite collocation points / targets are flagged, not hidden, on the tensor-core path too
+    (the packed-pair generators clamp t = 1 - q^2 with a NaN-keeping max, so a NaN jet stays NaN)."""
+    torch = torch_mod
+    w = HI.WORKLOADS[key]
+    net, params = _make(w)
+    ps = _points(w)
+    bad = HI.PointSet(ps.interior[:300].copy(), ps.boundary[:40], ps.g_boundary[:40].copy(),
+                      None if ps.initial is None else ps.initial[:20],
+                      None if ps.g_initial is None else ps.g_initial[:20])
+    bad.interior[7, 0] = np.nan
+    bad.interior[123, 1] = np.nan        # (an infinite coordinate is just outside the grid: zero features)
+    bad.g_boundary[3] = np.inf
+    out = _loss_grad_gpu(torch, net, w, bad)
+    assert out[w.num_params() + 2] == 3.0
+    assert not np.isfinite(out[w.num_params()])
+    # the finite points alone give finite results
+    good = HI.PointSet(ps.interior[:300], ps.boundary[:40], ps.g_boundary[:40],
+                       None if ps.initial is None else ps.initial[:20],
+                       None if ps.g_initial is None else ps.g_initial[:20])
+    out = _loss_grad_gpu(torch, net, w, good)
+    assert out[w.num_params() + 2] == 0.0 and np.isfinite(out[: w.num_params() + 2]).all()
