@@ -443,7 +443,7 @@ def main():
     step_ms_local = ms
     share = (dom_ms / prof_steps) / step_ms_local if step_ms_local > 0 else None
     clock_mhz = pk["sm_max_mhz"]
-    # SIMT (FFMA) peak = 148 SMs x 128 FP32 lanes x 2 flop x SM clock; TF32 tensor = bf16 x (1.1/2.25)
+    # SIMT (FFMA) peak = 148 SMs x 128 FP32 lanes x 2 flop x SM clock
     n_sms = torch.cuda.get_device_properties(dev).multi_processor_count
     fp32_peak = n_sms * 128 * 2 * clock_mhz * 1e6 / 1e12
     bf16_peak = pk["bf16_sustained"]          # bf16x3 tcgen05 kernels run on the BF16 tensor pipe
