@@ -484,7 +484,9 @@ def main():
                    "seconds": dt}
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "strong",
-                "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                # fp32 FFMA kernels; the wide-layer contractions run bf16x3 (bf16 hi/lo operands, fp32 TMEM accumulate)
+                "vs_baseline": None, "dtype": "f32+bf16x3" if tensor_core_layers(w, args.engine) else "f32",
+                "data": "synthetic",
                 "config": {"workload": w.key, "name": w.name, "n_interior": n_int_g, "n_boundary_initial": n_bi_g,
                            "widths": list(w.widths), "G": w.G, "k": w.k, "m": w.m, "pde": w.pde,
                            "parallelism": f"dp{world}", "l2": "flushed between timed steps (256 MiB write)",
