@@ -173,8 +173,13 @@ __device__ __forceinline__ void tiny_point(const TinyNet& tn, const float* __res
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
             float v = 0.f;
+            if (bc.k == 3) {                     // the paper's / BASELINE's k: 4 candidates, not KMAX
 #pragma unroll
-            for (int rr = 0; rr < KMAX; ++rr) v = (rr <= bc.k && q - rr == n0) ? cr[rr] : v;
+              for (int rr = 0; rr < 4; ++rr) v = (q - rr == n0) ? cr[rr] : v;
+            } else {
+#pragma unroll
+              for (int rr = 0; rr < KMAX; ++rr) v = (rr <= bc.k && q - rr == n0) ? cr[rr] : v;
+            }
             V[q] = v;
           }
           const float tot = warp_sum_transpose<8>(V, lane);
@@ -184,8 +189,13 @@ __device__ __forceinline__ void tiny_point(const TinyNet& tn, const float* __res
 #pragma unroll
           for (int q = 0; q < 16; ++q) {
             float v = 0.f;
+            if (bc.k == 3) {                     // the paper's / BASELINE's k: 4 candidates, not KMAX
 #pragma unroll
-            for (int rr = 0; rr < KMAX; ++rr) v = (rr <= bc.k && q - rr == n0) ? cr[rr] : v;
+              for (int rr = 0; rr < 4; ++rr) v = (q - rr == n0) ? cr[rr] : v;
+            } else {
+#pragma unroll
+              for (int rr = 0; rr < KMAX; ++rr) v = (rr <= bc.k && q - rr == n0) ? cr[rr] : v;
+            }
             V[q] = v;
           }
           const float tot = warp_sum_transpose<16>(V, lane);
