@@ -326,3 +326,103 @@ def test_adam_one_step_closed_forms():
     np.testing.assert_allclose(t1 - th, -1e-3 * g / (np.abs(g) + 1e-8), rtol=1e-12)
     np.testing.assert_allclose(m, 0.1 * g, rtol=1e-15)
     np.testing.assert_allclose(v, 0.001 * g ** 2, rtol=1e-12)
+
+
+# ---------------------------------------------------------------- residual pins on exact PDE solutions
+def _burgers_travelling_wave(a, nu, c, A):
+    """Exact travelling-wave solution of u_t + a u u_x - nu u_xx = 0 (Eq. 5, with the
+    advection coefficient a): u = c - A tanh(a A (x - a c t) / (2 nu)).  Derived by integrating
+    the travelling-wave ODE once (-s u + a u^2/2 - nu u' = const): matching the tanh^2 and tanh
+    coefficients gives k = a A / (2 nu) and s = a c.  Returns sympy (x, t, u)."""
+    x, t = sp.symbols("x t")
+    u = c - A * sp.tanh(a * A * (x - a * c * t) / (2 * nu))
+    return x, t, u
+
+
+def _jet_of(u, x, t, P):
+    f = sp.lambdify((x, t), [u, sp.diff(u, x), sp.diff(u, t), sp.diff(u, x, 2), sp.diff(u, t, 2)], "numpy")
+    vals = [np.broadcast_to(np.asarray(v, np.float64), (len(P),)) for v in f(P[:, 0], P[:, 1])]
+    uu, ux, ut, uxx, utt = vals
+    return uu, np.stack([ux, ut], 1), np.stack([uxx, utt], 1)
+
+
+@pytest.mark.parametrize("a,nu", [(1.0, 0.01 / np.pi), (0.25, 0.001 / 16), (0.7, 0.05)])
+def test_burgers_residual_vanishes_on_exact_solution(a, nu):
+    """burgers_residual (Eq. 5; Eq. 7, P:213 is a = 1/4, visc = nu/16) is zero on an exact
+    solution of the same PDE while each of its three terms is O(1) there: a dropped term, a flipped
+    sign, adv and visc swapped, or u_tt read for u_xx (u_tt = (a c)^2 u_xx here) all fail."""
+    c, A = 0.3, 0.5
+    x, t, u = _burgers_travelling_wave(sp.Rational(a).limit_denominator(10 ** 9), sp.Rational(nu).limit_denominator(10 ** 12), c, A)
+    width = 2 * nu / (a * A)                              # the front's length scale
+    rng = np.random.default_rng(5)
+    tt = rng.uniform(0, 1, 64)
+    xx = a * c * tt + rng.uniform(-2, 2, 64) * width       # points inside the front
+    P = np.stack([xx, tt], 1)
+    uu, du, d2u = _jet_of(u, x, t, P)
+    r = O.burgers_residual(uu, du, d2u, a, nu)
+    scale = np.abs(du[:, 1]) + np.abs(a * uu * du[:, 0]) + np.abs(nu * d2u[:, 0])
+    assert np.median(np.abs(du[:, 1])) > 1e-2 * np.median(scale)   # every term is non-trivial
+    assert np.median(np.abs(nu * d2u[:, 0])) > 1e-2 * np.median(scale)
+    assert np.all(np.abs(r) <= 1e-9 * scale)
+    # the wrong-reading variants do not vanish
+    assert np.max(np.abs(du[:, 1] + a * uu * du[:, 0] + nu * d2u[:, 0]) / scale) > 0.1
+    assert np.max(np.abs(du[:, 1] + a * uu * du[:, 0] - nu * d2u[:, 1]) / scale) > 0.1
+    assert np.max(np.abs(du[:, 1] + nu * uu * du[:, 0] - a * d2u[:, 0]) / scale) > 0.1
+
+
+def test_burgers_paper_change_of_variables():
+    """y = (x + 5)/4 maps Eq. 5 with nu = 0.001 on [-5,5] to Eq. 7 (u_t + 1/4 u u_y -
+    nu/16 u_yy = 0) on [0, 2.5].  An exact solution of Eq. 5, composed with x = 4y - 5, is zero under
+    burgers_residual(adv=1/4, visc=nu/16) and not under (adv=1, visc=nu)."""
+    nu = sp.Rational(1, 1000)
+    x, t, u = _burgers_travelling_wave(1, nu, sp.Rational(3, 10), sp.Rational(1, 2))
+    y = sp.symbols("y")
+    w = u.subs(x, 4 * y - 5)
+    rng = np.random.default_rng(6)
+    tt = rng.uniform(0, 2.5, 64)
+    yy = (0.3 * tt + 5 + rng.uniform(-2, 2, 64) * 2 * 0.001 / 0.5) / 4
+    P = np.stack([yy, tt], 1)
+    ww, dw, d2w = _jet_of(w, y, t, P)
+    scale = np.abs(dw[:, 1]) + np.abs(0.25 * ww * dw[:, 0]) + np.abs(0.001 / 16 * d2w[:, 0])
+    r = O.burgers_residual(ww, dw, d2w, 0.25, 0.001 / 16)
+    assert np.all(np.abs(r) <= 1e-9 * scale)
+    r_wrong = O.burgers_residual(ww, dw, d2w, 1.0, 0.001)
+    assert np.max(np.abs(r_wrong) / scale) > 0.5
+
+
+def test_poisson_forcing_3d():
+    """BASELINE.json C5: f = -3 pi^2 prod_j sin(pi x_j).  At (1/2,1/2,1/2) f = -3 pi^2, so the residual
+    of u == 0 is 3 pi^2; the exact solution prod_j sin(pi x_j) (laplacian -3 pi^2 prod sin) has zero
+    residual; f vanishes on every face x_j = 0 of the inner cross."""
+    half = np.array([[0.5, 0.5, 0.5]])
+    assert O.poisson_forcing(half)[0] == pytest.approx(-3 * np.pi ** 2, rel=1e-15)
+    assert O.poisson_residual(None, np.zeros((1, 3)), half)[0] == pytest.approx(3 * np.pi ** 2, rel=1e-15)
+    assert O.poisson_forcing(np.array([[-0.5, 0.5, 0.5]]))[0] == pytest.approx(3 * np.pi ** 2, rel=1e-15)
+    assert O.poisson_forcing(np.array([[0.3, 0.0, -0.7]]))[0] == 0.0
+    P = np.random.default_rng(1).uniform(-1, 1, (200, 3))
+    s = np.prod(np.sin(np.pi * P), axis=1)
+    d2 = np.stack([-np.pi ** 2 * s] * 3, 1)
+    assert np.abs(O.poisson_residual(None, d2, P)).max() < 1e-12
+    # a 2-D forcing applied to 3-D points would carry 2 pi^2, not 3 pi^2
+    assert abs(O.poisson_forcing(half)[0] + 2 * np.pi ** 2) > 1.0
+
+
+def test_adam_constant_gradient_every_step():
+    """with a constant gradient g, m_t = (1-b1^t) g and v_t = (1-b2^t) g^2, so the bias-corrected
+    step is -lr g / (|g| + eps) at EVERY t (a bias correction frozen at t = 1, or missing, fails from t = 2)."""
+    th0 = np.array([0.5, -1.0, 2.0, 0.0])
+    g = np.array([0.3, -2.0, 1e-3, 5.0])
+    th, m, v = th0.copy(), np.zeros(4), np.zeros(4)
+    lr, eps = 1e-2, 1e-8
+    for t in range(1, 6):
+        prev = th
+        th, m, v = O.adam_step(th, g, m, v, t, lr=lr, eps=eps)
+        np.testing.assert_allclose(th - prev, -lr * g / (np.abs(g) + eps), rtol=1e-9)
+        np.testing.assert_allclose(m, (1 - 0.9 ** t) * g, rtol=1e-12)
+        np.testing.assert_allclose(v, (1 - 0.999 ** t) * g ** 2, rtol=1e-9)
+    # a sign-alternating gradient: the first moment averages it, the step shrinks below lr
+    th, m, v = th0.copy(), np.zeros(4), np.zeros(4)
+    for t in range(1, 6):
+        prev = th
+        th, m, v = O.adam_step(th, (-1) ** t * g, m, v, t, lr=lr, eps=eps)
+    assert np.all(np.abs(th - prev) < lr)
