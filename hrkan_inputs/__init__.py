@@ -82,6 +82,13 @@ WORKLOADS: Dict[str, Workload] = {
                    1 << 22, 1 << 14, 1 << 14),
     "C5": Workload("C5", "poisson3d_[3,256,256,1]_G16_k3_m4", "poisson", (3, 256, 256, 1), 16, 3, 4,
                    1 << 24, 1 << 16, 0),
+    # the paper's own experiments (parity cases, not bench lines): Sec. 4.1 Poisson (PAPER.md:110-142,
+    # [2,2,1], g=5, 960 random interior + 4 x 30 equally spaced boundary points) and Sec. 4.2 transformed
+    # Burgers (Eq. 7: adv = 1/4, visc = nu/16, nu = 0.001, (y,t) in [0,2.5]^2,
+    # [2,3,3,3,1], g=7, 10000 interior + 100 + 100 boundary + 100 initial points, u(y,0) = 1/cosh(4y-5))
+    "PP": Workload("PP", "paper_poisson_[2,2,1]_G5_k3_m4", "poisson", (2, 2, 1), 5, 3, 4, 960, 120, 0),
+    "PB": Workload("PB", "paper_burgers_[2,3,3,3,1]_G7_k3_m4", "burgers", (2, 3, 3, 3, 1), 7, 3, 4, 10000, 200, 100,
+                   lo=0.0, hi=2.5, adv=0.25, visc=0.001 / 16),
 }
 
 
@@ -130,6 +137,19 @@ def _edges_2d(n_per_edge: int) -> np.ndarray:
 
 def make_points(w: Workload, seed: int = POINT_SEED) -> PointSet:
     rng = np.random.Generator(np.random.PCG64(seed))
+    if w.key.startswith("PP"):
+        interior = rng.uniform(-1.0, 1.0, size=(w.n_int, 2))
+        bnd = _edges_2d(w.n_bnd // 4)
+        return PointSet(_f32(interior), _f32(bnd), np.zeros(len(bnd), np.float32))
+    if w.key.startswith("PB"):
+        interior = rng.uniform(w.lo, w.hi, size=(w.n_int, 2))
+        nb = w.n_bnd // 2
+        tb = np.linspace(w.lo, w.hi, nb)
+        bnd = np.concatenate([np.stack([np.full(nb, w.lo), tb], 1), np.stack([np.full(nb, w.hi), tb], 1)], 0)
+        y0 = np.linspace(w.lo, w.hi, w.n_ic)
+        ic32 = _f32(np.stack([y0, np.zeros_like(y0)], 1))
+        g0 = _f32(1.0 / np.cosh(4.0 * ic32[:, 0].astype(np.float64) - 5.0))   # u(y,0) = 1/cosh(4y-5)
+        return PointSet(_f32(interior), _f32(bnd), np.zeros(len(bnd), np.float32), ic32, g0)
     if w.key.startswith("C1"):
         n = int(round(math.sqrt(w.n_int)))
         c = -1.0 + (2.0 * np.arange(n) + 1.0) / n            # cell-centred grid

@@ -85,3 +85,87 @@ def test_gloo_world2_matches_unsharded():
                                   n_bi_global=len(sets["boundary"]) + len(sets["initial"]), **sets).numpy()
     np.testing.assert_array_equal(res[0], res[1])          # identical on every rank
     np.testing.assert_allclose(res[0], ref, rtol=1e-10, atol=1e-14)
+
+
+# ------------------------------------------------------------------ bench.py's own DP step and launcher
+def _dp_step_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import bench
+        from paper_2409_14248_b200.parallel import DPTrainStep, check_replicas, global_counts
+        w = HI.WORKLOADS["C2"]
+        ps = HI.make_points(w).subset(7, 3)
+        sh = ps.shard(rank, world)
+        n_int, n_bi = global_counts({"interior": ps.interior, "boundary": ps.boundary, "initial": ps.initial})
+        net = bench.StubNet(2, seed=1)
+        t = lambda a: None if a is None else torch.from_numpy(a)
+        sets = {"interior": t(sh.interior), "boundary": t(sh.boundary), "g_boundary": t(sh.g_boundary),
+                "initial": t(sh.initial), "g_initial": t(sh.g_initial)}
+        out = torch.empty(net.n_params + 4)
+        step = DPTrainStep(net, None, sets, n_int, n_bi, out, world=world, lr=1e-2)
+        same0, _ = check_replicas(net, world)
+        grads = []
+        for _ in range(3):
+            grads.append(step().clone().numpy())
+        same1, dig = check_replicas(net, world)
+        q.put((rank, same0, same1, grads, net.get_params().numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_dp_train_step_world2_matches_single_process():
+    """DPTrainStep (the step bench.py times): 2 gloo ranks with a CPU stub net give the same allreduced
+    buffers and post-Adam parameters as one process over the whole set, and the replica digests agree."""
+    from bench import StubNet
+    from paper_2409_14248_b200.parallel import DPTrainStep
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_dp_step_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {r: rest for r, *rest in (q.get(timeout=300) for _ in range(world))}
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for r in range(world):
+        assert res[r][0] and res[r][1]                     # identical params after init and after steps
+    np.testing.assert_array_equal(res[0][3], res[1][3])
+    # single process over the whole set
+    w = HI.WORKLOADS["C2"]
+    ps = HI.make_points(w).subset(7, 3)
+    net = StubNet(2, seed=1)
+    t = lambda a: None if a is None else torch.from_numpy(a)
+    sets = {"interior": t(ps.interior), "boundary": t(ps.boundary), "g_boundary": t(ps.g_boundary),
+            "initial": t(ps.initial), "g_initial": t(ps.g_initial)}
+    out = torch.empty(net.n_params + 4)
+    step = DPTrainStep(net, None, sets, len(ps.interior), ps.n_bi, out, world=1, lr=1e-2)
+    for i in range(3):
+        g = step().clone().numpy()
+        np.testing.assert_allclose(res[0][2][i], g, rtol=2e-5, atol=1e-6)
+    np.testing.assert_allclose(res[0][3], net.get_params().numpy(), rtol=2e-5, atol=1e-6)
+
+
+def test_bench_launcher_dry_run_two_ranks():
+    """`bench.py --gpus 2 --dry-run` (no WORLD_SIZE): the launcher builds once, re-executes itself under
+    torch.distributed.run with 2 ranks (gloo + stub net on CPU), and rank 0 prints ONE JSON line with
+    n_gpus 2, one build in total, and bit-identical parameters on both ranks after the steps."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "HRKAN_BENCH_BUILT")}
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--dry-run", "--steps", "2",
+                        "--warmup", "1", "--config", "C2"], capture_output=True, text=True, timeout=600, env=env,
+                       cwd=root)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["comm"]["world_size"] == 2 and d["config"]["parallelism"] == "dp2"
+    assert d["builds"]["total"] == 1 and d["builds"]["per_rank"] == [0, 0]
+    assert d["replicas"]["params_identical_after_init"] and d["replicas"]["params_identical_after_steps"]
+    assert d["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0
