@@ -78,13 +78,32 @@ def class_flops(w: HI.Workload, n_int: int, n_bi: int, c_int: int):
 
 def tensor_core_layers(w: HI.Workload, engine: int) -> bool:
     """True when the hidden layers run on the tcgen05 kernels (libhrkan's tc_layer_ok rule)."""
+    if w.pde in ("kawahara", "aniso"):          # generic jet engine: band-limited FFMA on every layer
+        return False
     hidden = [(w.widths[l], w.widths[l + 1]) for l in range(1, len(w.widths) - 2)]
     return engine != 1 and bool(hidden) and all(O in (64, 128, 256) and I % 8 == 0 and
                                                 (engine == 2 or I * w.B >= 256) and w.B >= 8 for I, O in hidden)
 
 
 def interior_channels(w: HI.Workload) -> int:
-    return 1 + 2 + 1 if w.pde == "burgers" else 1 + 2 * w.D
+    """Jet channels of the interior pass: Burgers (u, u_x, u_t, u_xx), Poisson 1 + 2D, Kawahara the Taylor-5
+    jet (7), anisotropic the full Hessian jet 1 + D + D(D+1)/2."""
+    if w.pde == "burgers":
+        return 4
+    if w.pde == "kawahara":
+        return 7
+    if w.pde == "aniso":
+        return 1 + w.D + w.D * (w.D + 1) // 2
+    return 1 + 2 * w.D
+
+
+def pde_of(w: HI.Workload):
+    from paper_2409_14248_b200 import pde_struct
+    if w.pde == "kawahara":
+        return pde_struct("kawahara", w.alpha, adv=w.adv, disp3=w.disp3, disp5=w.disp5)
+    if w.pde == "aniso":
+        return pde_struct("aniso", w.alpha, aniso=list(w.aniso))
+    return pde_struct(w.pde, w.alpha, w.adv, w.visc)
 
 
 # ------------------------------------------------------------------------------------------
@@ -240,8 +259,17 @@ def _oracle_job(wkey: str, m: int, interior, bi, gbi, n_int_global: int, n_bi_gl
     """One shard of the oracle loss+grad (runs in a pool worker or in-process)."""
     from oracle import hrkan_oracle as O
     w = HI.WORKLOADS[wkey].with_m(m) if m != HI.WORKLOADS[wkey].m else HI.WORKLOADS[wkey]
-    net = O.Net(w.widths, w.G, w.k, w.m, w.lo, w.hi)
     params = HI.random_params(w.widths, w.G, w.k, seed=HI.PARAM_SEED)
+    if w.pde in ("kawahara", "aniso"):            # higher-order / mixed jets: the torch float64 oracle
+        from oracle import hrkan_oracle_jets as OJ
+        net = OJ.Net(w.widths, w.G, w.k, w.m, w.lo, w.hi)
+        pde = ({"kind": "kawahara", "alpha": w.alpha, "adv": w.adv, "disp3": w.disp3, "disp5": w.disp5}
+               if w.pde == "kawahara" else {"kind": "aniso", "alpha": w.alpha, "K": list(w.aniso)})
+        f = HI.aniso_forcing(interior, w) if w.pde == "aniso" else None
+        lp, lb, g = OJ.loss_grad(net, [(a.astype(np.float64), b.astype(np.float64)) for a, b in params], pde,
+                                 interior, bi, gbi, n_int_global=n_int_global, n_bi_global=n_bi_global, forcing=f)
+        return lp + lb
+    net = O.Net(w.widths, w.G, w.k, w.m, w.lo, w.hi)
     pde = {"kind": w.pde, "alpha": w.alpha, "adv": w.adv, "visc": w.visc}
     lp, lb, g = O.loss_grad(net, params, pde, interior, bi, gbi, n_int_global=n_int_global, n_bi_global=n_bi_global)
     return lp + lb
@@ -461,7 +489,7 @@ class StubNet:
     @staticmethod
     def _phi(x):
         import torch
-        return torch.cat([torch.ones(len(x), 1), x, x * x], 1)
+        return torch.cat([torch.ones(len(x), 1, dtype=x.dtype), x, x * x], 1)
 
     def pinn_loss_grad(self, pde, interior, boundary, g_boundary, initial=None, g_initial=None, forcing=None,
                        n_int_global=None, n_bi_global=None, out=None):
@@ -522,14 +550,14 @@ def run_rank(args):
         stream = None
     else:
         import __graft_entry__  # noqa: F401  (the library is built; load it)
-        from paper_2409_14248_b200 import HRKANNet, load_library, pde_struct
+        from paper_2409_14248_b200 import HRKANNet, load_library
         load_library()
         dev = torch.device(f"cuda:{local}")
         net = HRKANNet(w.widths, w.G, w.k, w.m, w.lo, w.hi, seed=HI.PARAM_SEED, device=local)
         net.set_engine(args.engine)
         if args.chunk:
             net.set_chunk_points(args.chunk)
-        pde = pde_struct(w.pde, w.alpha, w.adv, w.visc)
+        pde = pde_of(w)
         graph = (w.key in ("C1", "C2")) if args.graph < 0 else bool(args.graph)
         # graph replay needs a non-legacy stream; eager runs use the current stream
         stream = torch.cuda.Stream(device=dev) if graph else torch.cuda.current_stream()
@@ -538,7 +566,7 @@ def run_rank(args):
     same0, _ = check_replicas(net, world)
     cu = lambda a: None if a is None else torch.from_numpy(a).to(dev)
     dsets = {"interior": cu(sh.interior), "boundary": cu(sh.boundary), "g_boundary": cu(sh.g_boundary),
-             "initial": cu(sh.initial), "g_initial": cu(sh.g_initial)}
+             "initial": cu(sh.initial), "g_initial": cu(sh.g_initial), "forcing": cu(sh.forcing)}
     npar = net.n_params
     out = torch.empty(npar + 4, dtype=torch.float32, device=dev)
     step = DPTrainStep(net, pde, dsets, n_int_g, n_bi_g, out, world=world)
@@ -599,7 +627,7 @@ def run_rank(args):
         pin = (lambda a: None if a is None else torch.from_numpy(a)) if dry else \
               (lambda a: None if a is None else torch.from_numpy(a).pin_memory())
         hsets = {"interior": pin(sh.interior), "boundary": pin(sh.boundary), "g_boundary": pin(sh.g_boundary),
-                 "initial": pin(sh.initial), "g_initial": pin(sh.g_initial)}
+                 "initial": pin(sh.initial), "g_initial": pin(sh.g_initial), "forcing": pin(sh.forcing)}
         res = torch.empty(4, dtype=torch.float32)
         res = res if dry else res.pin_memory()
         h2d = sum(x.numel() * 4 for x in hsets.values() if x is not None)

@@ -52,6 +52,9 @@ class Workload:
     alpha: float = 0.05         # PAPER.md:142 / :239
     adv: float = 1.0            # Burgers r = u_t + adv*u*u_x - visc*u_xx (BASELINE.json form)
     visc: float = 0.01 / math.pi
+    disp3: float = 0.0          # Kawahara r = u_t + adv u u_x + disp3 u_xxx - disp5 u_xxxxx
+    disp5: float = 0.0
+    aniso: tuple = ()           # anisotropic r = sum_{a<=b} aniso[q] u_ab - f (upper triangle, row-major)
 
     @property
     def D(self) -> int:
@@ -89,6 +92,18 @@ WORKLOADS: Dict[str, Workload] = {
     "PP": Workload("PP", "paper_poisson_[2,2,1]_G5_k3_m4", "poisson", (2, 2, 1), 5, 3, 4, 960, 120, 0),
     "PB": Workload("PB", "paper_burgers_[2,3,3,3,1]_G7_k3_m4", "burgers", (2, 3, 3, 3, 1), 7, 3, 4, 10000, 200, 100,
                    lo=0.0, hi=2.5, adv=0.25, visc=0.001 / 16),
+    # SURVEY §8(f) row 3 (higher-order and mixed jets; PAPER.md:102 picks m = 6 for a u_xxxxx term):
+    #   K*: Kawahara u_t + u u_x + 0.01 u_xxx - 1e-4 u_xxxxx = 0 on [-1,1] x [0,1], exact solitary-wave
+    #       initial and boundary values (Taylor-5 jet); A*: anisotropic operator with mixed second
+    #       derivatives, manufactured u* = prod sin(pi x_a), forcing from u*, u = 0 on the boundary.
+    "K1": Workload("K1", "kawahara_[2,16,16,1]_G8_k3_m6", "kawahara", (2, 16, 16, 1), 8, 3, 6, 4096, 256, 256,
+                   adv=1.0, visc=0.0, disp3=0.01, disp5=1e-4),
+    "K6": Workload("K6", "kawahara_[2,64,64,1]_G10_k3_m6", "kawahara", (2, 64, 64, 1), 10, 3, 6, 1 << 20, 1 << 12,
+                   1 << 12, adv=1.0, visc=0.0, disp3=0.01, disp5=1e-4),
+    "A2": Workload("A2", "aniso2d_[2,32,32,1]_G8_k3_m4", "aniso", (2, 32, 32, 1), 8, 3, 4, 4096, 256, 0,
+                   aniso=(1.0, 0.6, 0.5)),
+    "A3": Workload("A3", "aniso3d_[3,32,32,1]_G8_k3_m6", "aniso", (3, 32, 32, 1), 8, 3, 6, 4096, 384, 0,
+                   aniso=(1.0, 0.4, 0.2, 0.8, 0.3, 0.6)),
 }
 
 
@@ -99,6 +114,7 @@ class PointSet:
     g_boundary: np.ndarray                # [Nb]    float32
     initial: Optional[np.ndarray] = None  # [N0, D] float32 (Burgers)
     g_initial: Optional[np.ndarray] = None
+    forcing: Optional[np.ndarray] = None  # [Ni] float32 (anisotropic operator: f of the manufactured solution)
 
     @property
     def n_bi(self) -> int:
@@ -109,7 +125,8 @@ class PointSet:
         return PointSet(
             self.interior[::s_int].copy(), self.boundary[::s_bi].copy(), self.g_boundary[::s_bi].copy(),
             None if self.initial is None else self.initial[::s_bi].copy(),
-            None if self.g_initial is None else self.g_initial[::s_bi].copy())
+            None if self.g_initial is None else self.g_initial[::s_bi].copy(),
+            None if self.forcing is None else self.forcing[::s_int].copy())
 
     def shard(self, rank: int, world: int) -> "PointSet":
         """Contiguous equal blocks per rank (the DP partition of SURVEY.md §8(e))."""
@@ -121,7 +138,7 @@ class PointSet:
             hi = (n * (rank + 1)) // world
             return a[lo:hi]
         return PointSet(blk(self.interior), blk(self.boundary), blk(self.g_boundary),
-                        blk(self.initial), blk(self.g_initial))
+                        blk(self.initial), blk(self.g_initial), blk(self.forcing))
 
 
 def _f32(a) -> np.ndarray:
@@ -135,8 +152,54 @@ def _edges_2d(n_per_edge: int) -> np.ndarray:
                            np.stack([t, -one], 1), np.stack([t, one], 1)], 0)
 
 
+def kawahara_wave(x, t, w: Workload, x0: float = -0.1):
+    """Exact solitary wave of u_t + a u u_x + b u_xxx - c u_xxxxx = 0 (data for the K* targets):
+    u = 105 b^2/(169 a c) sech^4( sqrt(b/(13 c))/2 (x - x0 - 36 b^2 t/(169 c)) )."""
+    a, b, c = w.adv, w.disp3, w.disp5
+    A = 105.0 * b * b / (169.0 * a * c)
+    kap = 0.5 * math.sqrt(b / (13.0 * c))
+    V = 36.0 * b * b / (169.0 * c)
+    return A / np.cosh(kap * (np.asarray(x, np.float64) - x0 - V * np.asarray(t, np.float64))) ** 4
+
+
+def aniso_forcing(P, w: Workload):
+    """f = sum_{a<=b} K_ab d_a d_b u* of the manufactured u* = prod_a sin(pi x_a) (data for the A* sets)."""
+    P = np.asarray(P, np.float64)
+    D = P.shape[1]
+    s, c = np.sin(np.pi * P), np.cos(np.pi * P)
+    pairs = [(a, b) for a in range(D) for b in range(a, D)]
+    f = np.zeros(len(P))
+    for q, (a, b) in enumerate(pairs):
+        if a == b:
+            d2 = -np.pi ** 2 * np.prod(s, 1)
+        else:
+            rest = np.prod(np.delete(s, [a, b], axis=1), 1) if D > 2 else 1.0
+            d2 = np.pi ** 2 * c[:, a] * c[:, b] * rest
+        f += w.aniso[q] * d2
+    return f
+
+
 def make_points(w: Workload, seed: int = POINT_SEED) -> PointSet:
     rng = np.random.Generator(np.random.PCG64(seed))
+    if w.pde == "kawahara":
+        x = rng.uniform(-1.0, 1.0, size=w.n_int)
+        t = rng.uniform(0.0, 1.0, size=w.n_int)
+        nb = w.n_bnd // 2
+        tb = np.linspace(0.0, 1.0, nb)
+        bnd = _f32(np.concatenate([np.stack([-np.ones(nb), tb], 1), np.stack([np.ones(nb), tb], 1)], 0))
+        x0 = np.linspace(-1.0, 1.0, w.n_ic)
+        ic = _f32(np.stack([x0, np.zeros_like(x0)], 1))
+        return PointSet(_f32(np.stack([x, t], 1)), bnd, _f32(kawahara_wave(bnd[:, 0], bnd[:, 1], w)), ic,
+                        _f32(kawahara_wave(ic[:, 0], ic[:, 1], w)))
+    if w.pde == "aniso":
+        interior = _f32(rng.uniform(-1.0, 1.0, size=(w.n_int, w.D)))
+        if w.D == 2:
+            bnd = _edges_2d(w.n_bnd // 4)
+        else:
+            q = np.arange(w.n_bnd)
+            bnd = rng.uniform(-1.0, 1.0, size=(w.n_bnd, 3))
+            bnd[q, (q % 6) // 2] = np.where(q % 2 == 0, -1.0, 1.0)
+        return PointSet(interior, _f32(bnd), np.zeros(len(bnd), np.float32), forcing=_f32(aniso_forcing(interior, w)))
     if w.key.startswith("PP"):
         interior = rng.uniform(-1.0, 1.0, size=(w.n_int, 2))
         bnd = _edges_2d(w.n_bnd // 4)

@@ -58,14 +58,33 @@ typedef enum {
   HRKAN_ENONFINITE = 5     /* reserved: non-finite values are reported through out[] flag     */
 } hrkan_status;
 
-typedef enum { HRKAN_POISSON = 0, HRKAN_BURGERS = 1 } hrkan_pde_kind;
+typedef enum {
+  HRKAN_POISSON = 0,   /* r = sum_a u_aa - f (Eq. 3)                                           */
+  HRKAN_BURGERS = 1,   /* r = u_t + adv u u_x - visc u_xx (Eq. 5; Eq. 7), D = 2 (x, t)     */
+  HRKAN_KAWAHARA = 2,  /* r = u_t + adv u u_x + disp3 u_xxx - disp5 u_xxxxx, D = 2 (x, t): a PDE with a
+                          fifth derivative ("u_xxxxx ... pick m to be larger, like 6"); m >= 3
+                          (v^(5) is non-zero for 2m >= 5 and continuous for m >= 6)                   */
+  HRKAN_ANISO = 3      /* r = sum_{a<=b} aniso[q(a,b)] u_ab - f with mixed second derivatives (full
+                          Hessian); q runs over the upper triangle row-major:
+                          D=2 (xx, xy, yy), D=3 (xx, xy, xz, yy, yz, zz); forcing f required          */
+} hrkan_pde_kind;
 
 typedef struct {
   int32_t kind;   /* hrkan_pde_kind                                                         */
   float alpha;    /* weight of L_pde (paper: 0.05, P:142 / P:239)                            */
   float adv;      /* Burgers: r = u_t + adv*u*u_x - visc*u_xx  (coordinates (x, t))         */
   float visc;     /*   BASELINE.json: adv = 1, visc = 0.01/pi;  paper Eq. 7: 1/4, 0.001/16   */
+  float disp3;    /* Kawahara: coefficient of u_xxx                                         */
+  float disp5;    /* Kawahara: coefficient of -u_xxxxx                                      */
+  float aniso[6]; /* HRKAN_ANISO: coefficients of u_ab over the upper triangle (a <= b)     */
 } hrkan_pde;
+
+/* Jet kinds of hrkan_forward_jet_ex (higher-order and mixed jets). */
+typedef enum {
+  HRKAN_JET_TAYLOR5 = 1,  /* D = 2 (x, t): C = 7 channels [u, u_x, u_xx, u_xxx, u_xxxx, u_xxxxx, u_t]        */
+  HRKAN_JET_HESSIAN = 2   /* D = 2 or 3: C = 1 + D + D(D+1)/2 channels [u, u_a (a < D), u_ab (a <= b, upper
+                             triangle row-major)] -- the full Hessian, mixed terms included                 */
+} hrkan_jet_kind;
 
 /* Create a network.  widths[0..n_widths-1] (host) = [D, hidden..., 1]; basis G (grid
  * intervals), k (B-spline order giving G+k supports), m (HR order, Eq. 2), [grid_lo, grid_hi]
@@ -97,9 +116,17 @@ hrkan_status hrkan_init_params(hrkan_net_t net, uint64_t seed, void* stream);
 hrkan_status hrkan_forward_jet(hrkan_net_t net, const float* pts, int64_t P,
                                float* u, float* du, float* d2u, void* stream);
 
+/* Higher-order / mixed jet of the network at P points pts[P, D]: jet[P][C] with the
+ * channels of `kind` (see hrkan_jet_kind), all exact derivatives of the network function u(xi).  The
+ * layers compose the jet channel by channel: Faa di Bruno's formula with the partial Bell polynomials for
+ * the x-orders (TAYLOR5), the second-order chain rule z_ab = phi'' h_a h_b + phi' h_ab (HESSIAN).
+ * EINVAL: P < 0, NULL pointers with P > 0, unknown kind, TAYLOR5 with D != 2 or m < 3, HESSIAN with D = 1.
+ * EUNSUPPORTED: a width above 256.  P = 0 is a no-op. */
+hrkan_status hrkan_forward_jet_ex(hrkan_net_t net, int32_t kind, const float* pts, int64_t P, float* jet, void* stream);
+
 /* One PINN loss + gradient evaluation.
  *   interior[Ni, D]  collocation points; forcing[Ni] = f (Poisson) or NULL for the built-in
- *                    f = -D pi^2 prod sin(pi xi_a); ignored for Burgers.
+ *                    f = -D pi^2 prod sin(pi xi_a); ignored for Burgers and Kawahara; required for ANISO.
  *   boundary[Nb, D], g_boundary[Nb]  boundary points and targets;
  *   initial[N0, D],  g_initial[N0]   initial-condition points and targets (may be NULL if N0=0).
  *   Ni_global, Nbi_global: the normalisers N_int and N_bi = Nb + N0 of the WHOLE job.  Pass the
@@ -108,9 +135,12 @@ hrkan_status hrkan_forward_jet(hrkan_net_t net, const float* pts, int64_t P,
  *   out[num_params + 4]: out[0..np-1] = dL/dtheta (OVERWRITTEN, flat layout), out[np] = alpha*L_pde
  *   part, out[np+1] = L_bi part, out[np+2] = non-finite flag (count of non-finite residuals /
  *   boundary errors; summed by an allreduce so any rank's flag shows), out[np+3] = 0 (pad).
- * Burgers requires D = 2 (coordinates (x, t)).
+ * Burgers and Kawahara require D = 2 (coordinates (x, t)); Kawahara m >= 3; ANISO D = 2 or 3 and a forcing.
+ * The interior pass of KAWAHARA / ANISO runs the generic jet engine (band-limited FFMA kernels on the
+ * TAYLOR5 / HESSIAN jets); boundary and initial points always run the value-only kernels.
  * EINVAL: negative counts, NULL pointer with non-zero count, Ni_global < Ni, Nbi_global < Nb+N0,
- *         Burgers with D != 2, unknown pde kind, out == NULL. */
+ *         Burgers/Kawahara with D != 2, Kawahara with m < 3, ANISO with D = 1 or no forcing, unknown pde
+ *         kind, out == NULL. */
 hrkan_status hrkan_pinn_loss_grad(hrkan_net_t net, const hrkan_pde* pde,
                                   const float* interior, const float* forcing, int64_t Ni,
                                   const float* boundary, const float* g_boundary, int64_t Nb,
@@ -119,8 +149,11 @@ hrkan_status hrkan_pinn_loss_grad(hrkan_net_t net, const hrkan_pde* pde,
                                   float* out, void* stream);
 
 /* One bias-corrected Adam step on the net's parameters with gradient grad[num_params]
- * (t += 1 first; m = b1 m + (1-b1) g; v = b2 v + (1-b2) g^2; theta -= lr mhat/(sqrt(vhat)+eps)).
- * EINVAL: grad == NULL, lr/eps not finite, beta outside [0,1). */
+ * (t += 1 first; m = b1 m + (1-b1) g; v = b2 v + (1-b2) g^2; theta -= lr mhat/(sqrt(vhat)+eps),
+ * mhat = m/(1-b1^t), vhat = v/(1-b2^t); "Adam optimizer").  The step count t lives in
+ * device memory and is advanced by the kernel itself, so a caller's CUDA-graph capture of a whole
+ * training step (loss+grad, allreduce, Adam) replays with a live bias correction.  hrkan_init_params
+ * resets t to 0.  EINVAL: grad == NULL, lr/eps not finite, beta outside [0,1). */
 hrkan_status hrkan_adam_step(hrkan_net_t net, const float* grad, float lr, float beta1, float beta2,
                              float eps, void* stream);
 
@@ -128,7 +161,7 @@ hrkan_status hrkan_adam_step(hrkan_net_t net, const float* grad, float lr, float
  * workspace, SURVEY §7 hard part (f)).  0 = default.  EINVAL: chunk < 0. */
 hrkan_status hrkan_set_chunk_points(hrkan_net_t net, int64_t chunk);
 
-/* Select the engine: 0 = auto (one-launch fused kernel for tiny nets -- every width <= 8, <= 4 layers,
+/* Select the engine (a change re-derives every kernel-private weight copy before the next call): 0 = auto (one-launch fused kernel for tiny nets -- every width <= 8, <= 4 layers,
  * <= 2048 parameters, k <= 7; its last block reduces the gradient -- else tcgen05 tensor cores where a
  * hidden layer is wide (O in {64,128,256}, I % 8 == 0, G+k >= 8) and SIMT FFMA elsewhere), 1 = force the
  * layered SIMT FFMA kernels, 2 = force tcgen05 where supported (layered).
@@ -141,7 +174,9 @@ hrkan_status hrkan_set_engine(hrkan_net_t net, int32_t mode);
  * chunk size, engine) runs eagerly, the second captures the whole call into a CUDA graph (weight
  * re-tiling included) and later calls replay it with one cudaGraphLaunch -- the launch-latency
  * bound small configs (C1, C2) become one graph launch per step.  Results are bitwise identical to
- * eager calls.  Changing any argument re-captures.  A caller's own stream capture (e.g. of a whole
+ * eager calls.  Changing any argument re-captures, and so does any growth of the library's workspace
+ * (e.g. an hrkan_forward_jet on more points than the training chunk between two steps): the graph's
+ * baked-in workspace pointers are never replayed after a reallocation.  A caller's own stream capture (e.g. of a whole
  * training step with the NCCL allreduce) simply records the eager launches.  EINVAL: net == NULL. */
 hrkan_status hrkan_set_graph_mode(hrkan_net_t net, int32_t enable);
 

@@ -231,7 +231,7 @@ def loss_grad(net: Net, params, pde: dict, pts_int, pts_bi, g_bi, n_int_global=N
     grads = torch.autograd.grad(L, flat, allow_unused=True)
     grads = [torch.zeros_like(t) if g is None else g for t, g in zip(flat, grads)]
     out = [(grads[2 * l].numpy(), grads[2 * l + 1].numpy()) for l in range(len(pt))]
-    return float(lp), float(lb), out
+    return float(lp.detach()), float(lb.detach()), out
 
 
 def flat_grad(grads) -> np.ndarray:

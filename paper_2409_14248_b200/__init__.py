@@ -6,4 +6,5 @@
            allreduce of the flat [dL/dtheta | loss parts | flag] buffer (torch.distributed,
            NCCL on GPUs, gloo in the CPU tests).
 """
-from .hrkan import HRKANNet, HrkanError, HrkanPde, load_library, pde_struct  # noqa: F401
+from .hrkan import (HRKANNet, HrkanError, HrkanPde, JET_HESSIAN, JET_TAYLOR5, jet_channels, load_library,  # noqa: F401
+                    pde_struct)

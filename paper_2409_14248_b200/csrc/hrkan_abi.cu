@@ -5,6 +5,7 @@
 // Every arithmetic step of the hot path runs in the kernels of simt_kernels.cuh, last_kernels.cuh
 // and tc_*.cuh; this file only validates arguments, owns device memory and sequences launches on
 // the caller's stream (SURVEY §3 "New build" call stack).
+#include <atomic>
 #include <cstdlib>
 
 #include "hrkan_internal.cuh"
@@ -14,6 +15,9 @@
 namespace hrkan {
 
 thread_local std::string g_err;
+static std::atomic<uint64_t> g_ws_gen{0};
+uint64_t workspace_generation() { return g_ws_gen.load(std::memory_order_relaxed); }
+void bump_workspace_generation() { g_ws_gen.fetch_add(1, std::memory_order_relaxed); }
 
 hrkan_status fail(hrkan_status s, const std::string& msg) {
   g_err = msg;
@@ -35,6 +39,7 @@ hrkan_status refresh_derived(hrkan_net* net, cudaStream_t st, bool force = false
   }
   HR_TRY(tc_refresh_weights(net, st));
   net->derived_dirty = false;
+  net->body_refreshed = true;
   return HRKAN_OK;
 }
 
@@ -81,6 +86,19 @@ hrkan_status dispatch_pass(hrkan_net* net, int nf, int ns, const PassArgs& a, cu
     case 6: return dispatch_pass_m6(net, nf, ns, a, st);
     case 7: return dispatch_pass_m7(net, nf, ns, a, st);
     case 8: return dispatch_pass_m8(net, nf, ns, a, st);
+  }
+  return fail(HRKAN_EINVAL, "m must be in [2, 8]");
+}
+
+hrkan_status dispatch_spec(hrkan_net* net, int spec, const PassArgs& a, cudaStream_t st) {
+  switch (net->m) {
+    case 2: return dispatch_spec_m2(net, spec, a, st);
+    case 3: return dispatch_spec_m3(net, spec, a, st);
+    case 4: return dispatch_spec_m4(net, spec, a, st);
+    case 5: return dispatch_spec_m5(net, spec, a, st);
+    case 6: return dispatch_spec_m6(net, spec, a, st);
+    case 7: return dispatch_spec_m7(net, spec, a, st);
+    case 8: return dispatch_spec_m8(net, spec, a, st);
   }
   return fail(HRKAN_EINVAL, "m must be in [2, 8]");
 }
@@ -162,7 +180,8 @@ hrkan_status hrkan_create(const int32_t* widths, int32_t n_widths, int32_t G, in
   };
   if (cudaMalloc(&net->params, sizeof(float) * off) != cudaSuccess ||
       cudaMalloc(&net->adam_m, sizeof(float) * off) != cudaSuccess ||
-      cudaMalloc(&net->adam_v, sizeof(float) * off) != cudaSuccess) {
+      cudaMalloc(&net->adam_v, sizeof(float) * off) != cudaSuccess ||
+      cudaMalloc(&net->adam_t, 2 * sizeof(int)) != cudaSuccess) {
     cudaGetLastError();
     return cleanup(fail(HRKAN_ENOMEM, "parameter allocation failed"));
   }
@@ -194,6 +213,9 @@ hrkan_status hrkan_set_chunk_points(hrkan_net_t net, int64_t chunk) {
 hrkan_status hrkan_set_engine(hrkan_net_t net, int32_t mode) {
   if (!net) return fail(HRKAN_EINVAL, "net is NULL");
   if (mode < 0 || mode > 2) return fail(HRKAN_EINVAL, "engine mode must be 0, 1 or 2");
+  // the engine decides which derived weight copies refresh_derived maintains (engine 1 skips the
+  // tensor-core tiles): any change re-derives all of them before the next call
+  if (mode != net->engine) net->derived_dirty = true;
   net->engine = mode;
   return HRKAN_OK;
 }
@@ -213,7 +235,7 @@ hrkan_status hrkan_init_params(hrkan_net_t net, uint64_t seed, void* stream) {
   }
   HR_CUDA(cudaMemsetAsync(net->adam_m, 0, sizeof(float) * net->n_params, st));
   HR_CUDA(cudaMemsetAsync(net->adam_v, 0, sizeof(float) * net->n_params, st));
-  net->adam_t = 0;
+  HR_CUDA(cudaMemsetAsync(net->adam_t, 0, 2 * sizeof(int), st));
   net->derived_dirty = true;
   return HRKAN_OK;
 }
@@ -267,6 +289,40 @@ hrkan_status hrkan_forward_jet(hrkan_net_t net, const float* pts, int64_t P, flo
   return HRKAN_OK;
 }
 
+hrkan_status hrkan_forward_jet_ex(hrkan_net_t net, int32_t kind, const float* pts, int64_t P, float* jet, void* stream) {
+  if (!net) return fail(HRKAN_EINVAL, "net is NULL");
+  if (P < 0) return fail(HRKAN_EINVAL, "P must be >= 0");
+  if (kind != HRKAN_JET_TAYLOR5 && kind != HRKAN_JET_HESSIAN) return fail(HRKAN_EINVAL, "unknown jet kind");
+  if (kind == HRKAN_JET_TAYLOR5 && (net->D != 2 || net->m < 3))
+    return fail(HRKAN_EINVAL, "the Taylor-5 jet needs D = 2 (x, t) and m >= 3");
+  if (kind == HRKAN_JET_HESSIAN && net->D < 2) return fail(HRKAN_EINVAL, "the Hessian jet needs D = 2 or 3");
+  if (P == 0) return HRKAN_OK;
+  if (!pts || !jet) return fail(HRKAN_EINVAL, "NULL pts / jet");
+  clear_error();
+  DeviceGuard dg(net->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int D = net->D;
+  const int C = kind == HRKAN_JET_TAYLOR5 ? 7 : 1 + D + D * (D + 1) / 2;
+  const float* dpts;
+  HR_TRY(stage_in(pts, P * D, net->st_pts, st, &dpts));
+  float* jet_dev = jet;
+  const bool hj = !is_device_ptr(jet);
+  if (hj) {
+    HR_CUDA(net->st_u.ensure(sizeof(float) * P * C));
+    jet_dev = net->st_u.f();
+  }
+  HR_TRY(refresh_derived(net, st));
+  PassArgs a{};
+  a.kind = PASS_JET;
+  a.pts = dpts;
+  a.P = P;
+  a.jet_out = jet_dev;
+  const int spec = kind == HRKAN_JET_TAYLOR5 ? JSPEC_TAYLOR5 : (D == 2 ? JSPEC_HESS2 : JSPEC_HESS3);
+  HR_TRY(dispatch_spec(net, spec, a, st));
+  if (hj) HR_CUDA(cudaMemcpyAsync(jet, jet_dev, sizeof(float) * P * C, cudaMemcpyDeviceToHost, st));
+  return HRKAN_OK;
+}
+
 }  // extern "C"
 
 namespace {
@@ -280,7 +336,7 @@ hrkan_status loss_grad_body(hrkan_net* net, const hrkan_pde* pde, const float* i
   const int64_t np = net->n_params;
   const float *d_int, *d_f = nullptr, *d_bnd, *d_gb, *d_ini, *d_gi;
   HR_TRY(stage_in(interior, Ni * D, net->st_int, st, &d_int));
-  if (forcing && pde->kind == HRKAN_POISSON) HR_TRY(stage_in(forcing, Ni, net->st_f, st, &d_f));
+  if (forcing && (pde->kind == HRKAN_POISSON || pde->kind == HRKAN_ANISO)) HR_TRY(stage_in(forcing, Ni, net->st_f, st, &d_f));
   HR_TRY(stage_in(boundary, Nb * D, net->st_bnd, st, &d_bnd));
   HR_TRY(stage_in(g_boundary, Nb, net->st_gb, st, &d_gb));
   HR_TRY(stage_in(initial, N0 * D, net->st_ini, st, &d_ini));
@@ -291,7 +347,7 @@ hrkan_status loss_grad_body(hrkan_net* net, const hrkan_pde* pde, const float* i
     HR_CUDA(net->st_out.ensure(sizeof(float) * (np + 4)));
     dout = net->st_out.f();
   }
-  if (tiny_eligible(net)) {
+  if (tiny_eligible(net) && (pde->kind == HRKAN_POISSON || pde->kind == HRKAN_BURGERS)) {
     TinyArgs t{pde, d_int, d_f, d_bnd, d_gb, d_ini, d_gi, Ni, Nb, N0, (float)(1.0 / (double)std::max<int64_t>(1, Ni_global)),
                Nbi_global > 0 ? (float)(1.0 / (double)Nbi_global) : 0.f, dout};
     HR_TRY(tiny_step(net, t, st));
@@ -311,8 +367,14 @@ hrkan_status loss_grad_body(hrkan_net* net, const hrkan_pde* pde, const float* i
     a.forcing = d_f;
     a.out_loss = dout + np;
     a.inv_n = (float)(1.0 / (double)Ni_global);
-    const int nf = D, ns = (pde->kind == HRKAN_BURGERS) ? 1 : D;
-    HR_TRY(dispatch_pass(net, nf, ns, a, st));
+    if (pde->kind == HRKAN_KAWAHARA) {
+      HR_TRY(dispatch_spec(net, JSPEC_TAYLOR5, a, st));
+    } else if (pde->kind == HRKAN_ANISO) {
+      HR_TRY(dispatch_spec(net, D == 2 ? JSPEC_HESS2 : JSPEC_HESS3, a, st));
+    } else {
+      const int nf = D, ns = (pde->kind == HRKAN_BURGERS) ? 1 : D;
+      HR_TRY(dispatch_pass(net, nf, ns, a, st));
+    }
   }
   a.kind = PASS_BOUNDARY;
   a.out_loss = dout + np + 1;
@@ -352,8 +414,13 @@ hrkan_status hrkan_pinn_loss_grad(hrkan_net_t net, const hrkan_pde* pde, const f
   if ((Ni > 0 && !interior) || (Nb > 0 && (!boundary || !g_boundary)) || (N0 > 0 && (!initial || !g_initial)))
     return fail(HRKAN_EINVAL, "NULL point/target buffer with a non-zero count");
   if (Ni_global < Ni || Nbi_global < Nb + N0) return fail(HRKAN_EINVAL, "global normalisers smaller than local counts");
-  if (pde->kind != HRKAN_POISSON && pde->kind != HRKAN_BURGERS) return fail(HRKAN_EINVAL, "unknown pde kind");
+  if (pde->kind < HRKAN_POISSON || pde->kind > HRKAN_ANISO) return fail(HRKAN_EINVAL, "unknown pde kind");
   if (pde->kind == HRKAN_BURGERS && net->D != 2) return fail(HRKAN_EINVAL, "Burgers needs D = 2 (x, t)");
+  if (pde->kind == HRKAN_KAWAHARA && net->D != 2) return fail(HRKAN_EINVAL, "Kawahara needs D = 2 (x, t)");
+  if (pde->kind == HRKAN_KAWAHARA && net->m < 3)
+    return fail(HRKAN_EINVAL, "u_xxxxx needs m >= 3 (v^(5) = 0 for m = 2; m >= 6 makes it continuous, P:102)");
+  if (pde->kind == HRKAN_ANISO && net->D < 2) return fail(HRKAN_EINVAL, "the anisotropic operator needs D = 2 or 3");
+  if (pde->kind == HRKAN_ANISO && Ni > 0 && !forcing) return fail(HRKAN_EINVAL, "the anisotropic operator needs a forcing");
   if (!std::isfinite(pde->alpha)) return fail(HRKAN_EINVAL, "alpha must be finite");
   clear_error();
   DeviceGuard dg(net->device);
@@ -380,11 +447,13 @@ hrkan_status hrkan_pinn_loss_grad(hrkan_net_t net, const hrkan_pde* pde, const f
   std::memcpy(key.ptrs, kp, sizeof(kp));
   key.n[0] = Ni; key.n[1] = Nb; key.n[2] = N0; key.n[3] = Ni_global; key.n[4] = Nbi_global; key.n[5] = net->chunk;
   key.kind = pde->kind; key.engine = net->engine;
-  key.f[0] = pde->alpha; key.f[1] = pde->adv; key.f[2] = pde->visc;
+  key.f[0] = pde->alpha; key.f[1] = pde->adv; key.f[2] = pde->visc; key.f[3] = pde->disp3; key.f[4] = pde->disp5;
+  for (int q = 0; q < 6; ++q) key.f[5 + q] = pde->aniso[q];
+  key.ws_gen = workspace_generation();
   if (net->graph_exec && same_key(key, net->graph_key)) {
     HR_CUDA(cudaGraphLaunch(net->graph_exec, st));
     net->launches += net->graph_launches;
-    net->derived_dirty = false;
+    if (net->graph_refreshes) net->derived_dirty = false;   // the tiny-net body never re-derives
     return HRKAN_OK;
   }
   if (!same_key(key, net->graph_key)) {           // new signature: run eagerly, capture next time
@@ -395,6 +464,8 @@ hrkan_status hrkan_pinn_loss_grad(hrkan_net_t net, const hrkan_pde* pde, const f
                           Nbi_global, out, st, false);
   }
   const int64_t l0 = net->launches;
+  const bool dirty0 = net->derived_dirty;
+  net->body_refreshed = false;
   HR_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
   const hrkan_status sb = loss_grad_body(net, pde, interior, forcing, Ni, boundary, g_boundary, Nb, initial, g_initial,
                                          N0, Ni_global, Nbi_global, out, st, true);
@@ -402,6 +473,8 @@ hrkan_status hrkan_pinn_loss_grad(hrkan_net_t net, const hrkan_pde* pde, const f
   const cudaError_t ec = cudaStreamEndCapture(st, &graph);
   net->graph_launches = net->launches - l0;
   net->launches = l0;
+  net->graph_refreshes = net->body_refreshed;
+  net->derived_dirty = dirty0;        // capture records launches without running them
   if (sb != HRKAN_OK || ec != cudaSuccess || !graph) {
     if (graph) cudaGraphDestroy(graph);
     cudaGetLastError();
@@ -416,9 +489,10 @@ hrkan_status hrkan_pinn_loss_grad(hrkan_net_t net, const hrkan_pde* pde, const f
     std::memset(&net->graph_key, 0, sizeof(GraphKey));
     return fail(HRKAN_ECUDA, std::string("cudaGraphInstantiate: ") + cudaGetErrorString(ei));
   }
+  net->graph_key.ws_gen = workspace_generation();   // capture itself never reallocates
   HR_CUDA(cudaGraphLaunch(net->graph_exec, st));
   net->launches += net->graph_launches;
-  net->derived_dirty = false;
+  if (net->graph_refreshes) net->derived_dirty = false;
   return HRKAN_OK;
 }
 
@@ -442,13 +516,10 @@ hrkan_status hrkan_adam_step(hrkan_net_t net, const float* grad, float lr, float
   cudaStream_t st = (cudaStream_t)stream;
   const float* dg_ptr;
   HR_TRY(stage_in(grad, net->n_params, net->st_out, st, &dg_ptr));
-  net->adam_t += 1;
-  const double bc1 = 1.0 - std::pow((double)beta1, (double)net->adam_t);
-  const double bc2 = 1.0 - std::pow((double)beta2, (double)net->adam_t);
   const int64_t n = net->n_params;
   HR_LAUNCH(HRKAN_K_ADAM, "k_adam",
             k_adam<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(net->params, net->adam_m, net->adam_v, dg_ptr, n, lr, beta1,
-                                                                beta2, eps, (float)(1.0 / bc1), (float)(1.0 / bc2)));
+                                                                beta2, eps, net->adam_t));
   net->derived_dirty = true;
   return HRKAN_OK;
 }
@@ -492,6 +563,7 @@ void hrkan_free(hrkan_net_t net) {
   cudaFree(net->params);
   cudaFree(net->adam_m);
   cudaFree(net->adam_v);
+  cudaFree(net->adam_t);
   for (float* p : net->wt) cudaFree(p);
   DevBuf* bufs[] = {&net->jets, &net->adj_a, &net->adj_b, &net->loss_part, &net->w_part, &net->b_part, &net->last_part, &net->first_part,
                     &net->st_int, &net->st_f, &net->st_bnd, &net->st_gb, &net->st_ini, &net->st_gi,

@@ -65,11 +65,18 @@ inline bool is_device_ptr(const void* p) {
   return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
 
+// Process-wide count of workspace reallocations.  A captured CUDA graph bakes in raw workspace
+// pointers, so the graph key of hrkan_pinn_loss_grad carries this generation and any reallocation
+// (e.g. a larger hrkan_forward_jet between training steps) forces a re-capture.
+uint64_t workspace_generation();
+void bump_workspace_generation();
+
 struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;
   cudaError_t ensure(size_t n) {
     if (n <= bytes) return cudaSuccess;
+    bump_workspace_generation();
     if (p) cudaFree(p);
     p = nullptr;
     bytes = 0;
@@ -101,7 +108,8 @@ using namespace hrkan;
 struct GraphKey {
   const void* ptrs[8];
   int64_t n[6];
-  float f[3];
+  uint64_t ws_gen;                     // workspace_generation() when the signature was recorded
+  float f[11];
   int32_t kind, engine;
 };
 
@@ -118,7 +126,8 @@ struct hrkan_net {
   float* params = nullptr;             // flat, owned
   float* adam_m = nullptr;
   float* adam_v = nullptr;
-  int64_t adam_t = 0;
+  int* adam_t = nullptr;               // device [t, finished-block counter]: k_adam increments t on the
+                                       // device, so a captured Adam step keeps its bias correction live
   std::vector<float*> wt;              // derived: W_l transposed to [I][B][O]
   bool derived_dirty = true;
   int64_t chunk = 0;                   // 0 = auto
@@ -142,6 +151,8 @@ struct hrkan_net {
   GraphKey graph_key{};
   cudaGraphExec_t graph_exec = nullptr;
   int64_t graph_launches = 0;
+  bool graph_refreshes = false;         // the captured body re-tiles the derived weight copies
+  bool body_refreshed = false;          // set by refresh_derived (capture bookkeeping)
   // device-time profiling (hrkan_profile_enable / hrkan_profile_read)
   struct ProfEv { cudaEvent_t a, b; int cls; };
   bool prof_on = false;
@@ -186,6 +197,17 @@ inline hrkan_status make_tmap_f32_3d(CUtensorMap* m, const float* base, uint64_t
                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(HRKAN_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
   return HRKAN_OK;
+}
+
+// Opt a kernel into `dyn` bytes of dynamic shared memory whenever its static + dynamic shared memory
+// exceeds the 48 KB default (the static part counts: k_wgrad_first at O = 128, D = 3 needs it).
+template <class K>
+inline cudaError_t smem_optin(K kfn, size_t dyn) {
+  cudaFuncAttributes fa;
+  cudaError_t e = cudaFuncGetAttributes(&fa, (const void*)kfn);
+  if (e != cudaSuccess) return e;
+  if (fa.sharedSizeBytes + dyn <= 48 * 1024) return cudaSuccess;
+  return cudaFuncSetAttribute((const void*)kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
 }
 
 inline int prof_pre(hrkan_net* net, cudaStream_t st) {
@@ -264,7 +286,11 @@ struct PassArgs {
   float* out_flag;
   const hrkan_pde* pde;
   float inv_n;             // 1/N_int_global or 1/N_bi_global
+  float* jet_out;          // PASS_JET of a generic jet spec: [P][C] output jet (device)
 };
+
+// Generic jet specs (jet_kernels.cuh)
+enum JetSpecId { JSPEC_TAYLOR5 = 0, JSPEC_HESS2 = 1, JSPEC_HESS3 = 2 };
 
 // Forward + (optional) loss/seeds + reverse over one point set, chunk by chunk.
 
@@ -280,7 +306,8 @@ struct TinyArgs {
 // One scheduler per HR order m (pass_m<m>.cu).
 #define HRKAN_DECLARE_DISPATCH(MM) \
   hrkan_status dispatch_pass_m##MM(hrkan_net* net, int nf, int ns, const PassArgs& a, cudaStream_t st); \
-  hrkan_status tiny_step_m##MM(hrkan_net* net, const TinyArgs& t, cudaStream_t st);
+  hrkan_status tiny_step_m##MM(hrkan_net* net, const TinyArgs& t, cudaStream_t st); \
+  hrkan_status dispatch_spec_m##MM(hrkan_net* net, int spec, const PassArgs& a, cudaStream_t st);
 HRKAN_DECLARE_DISPATCH(2)
 HRKAN_DECLARE_DISPATCH(3)
 HRKAN_DECLARE_DISPATCH(4)

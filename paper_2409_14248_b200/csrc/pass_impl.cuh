@@ -8,6 +8,7 @@
 #include "first_kernels.cuh"
 #include "tiny_kernels.cuh"
 #include "tc_kernels.cuh"
+#include "jet_kernels.cuh"
 
 namespace {
 
@@ -67,7 +68,7 @@ hrkan_status launch_last(hrkan_net* net, const float* in, int64_t n, const PassA
   }
   const size_t smem = sizeof(float) * (size_t)LF_WARPS * IB;
   if (smem > 200 * 1024) return fail(HRKAN_EUNSUPPORTED, "output layer too wide for the fused last-layer kernel");
-  if (smem > 48 * 1024) HR_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  HR_CUDA(smem_optin(kfn, smem));
   const int per_sm = std::max(1, std::min(4, (int)((220 * 1024) / std::max<size_t>(smem, 1))));
   const int nb = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)per_sm * net->num_sms, (n + LF_WARPS - 1) / LF_WARPS));
   HR_CUDA(net->last_part.ensure(sizeof(float) * (size_t)nb * (IB + 4)));
@@ -176,7 +177,7 @@ hrkan_status run_pass(hrkan_net* net, const PassArgs& a, cudaStream_t st) {
           const int QG = O <= FL_THREADS ? FL_THREADS / O : 1;
           const size_t fsm = sizeof(float) * (size_t)QG * I * net->B * O;
           if (fsm > 200 * 1024 || O > 2 * FL_THREADS) return fail(HRKAN_EUNSUPPORTED, "first layer too wide");
-          if (fsm > 48 * 1024) HR_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm));
+          HR_CUDA(smem_optin(kfn, fsm));
           const int bd = FL_THREADS;
           const int nzf = (int)std::max<int64_t>(1, std::min<int64_t>(2 * net->num_sms, n / 64));
           const int64_t nWf = (int64_t)O * I * net->B;
@@ -189,7 +190,7 @@ hrkan_status run_pass(hrkan_net* net, const PassArgs& a, cudaStream_t st) {
           continue;
         } else {
           auto kfn = k_wgrad_simt<NF, NS, M, false>;
-          if (smem > 48 * 1024) HR_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+          HR_CUDA(smem_optin(kfn, smem));
           HR_LAUNCH(cls, "k_wgrad_simt", kfn<<<grid, blk, smem, st>>>(in, ybar, net->w_part.f(), net->b_part.f(), n, I, O, bc));
         }
         const int64_t nW = (int64_t)O * I * net->B;
@@ -204,6 +205,124 @@ hrkan_status run_pass(hrkan_net* net, const PassArgs& a, cudaStream_t st) {
           HR_LAUNCH(HRKAN_K_DGRAD_HIDDEN, "k_dgrad_simt",
                     k_dgrad_simt<NF, NS, M><<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(in, net->params + net->w_off[l], ybar, xbar, n, I, O, bc));
         }
+        std::swap(ybar, xbar);
+      }
+    }
+  }
+  return HRKAN_OK;
+}
+
+// Forward + loss/seeds + reverse of a generic jet spec S (jet_kernels.cuh), chunk by
+// chunk: seeded layer-0 jet, every layer on the band-limited FFMA kernels, the Kawahara / anisotropic
+// residual of the output jet, then wgrad + input adjoint from the last layer to the first.
+template <class S, int M>
+hrkan_status run_pass_spec(hrkan_net* net, const PassArgs& a, cudaStream_t st) {
+  constexpr int C = S::C;
+  const int L = net->L, D = net->D;
+  if (D != S::D) return fail(HRKAN_EINVAL, "internal: jet spec dimension mismatch");
+  int64_t sumw = 0;
+  for (int l = 1; l <= L; ++l) sumw += net->widths[l];
+  const int maxw = std::max(net->max_width, D);
+  int64_t Pc = net->chunk;
+  if (Pc <= 0) {
+    Pc = (int64_t)(12.0e9 / (4.0 * C * (double)(sumw + 2 * maxw)));
+    Pc = std::max<int64_t>(256, std::min<int64_t>(Pc, 1 << 20) / 256 * 256);
+  }
+  Pc = std::min<int64_t>(Pc, std::max<int64_t>(a.P, 1));
+  for (int l = 0; l < L; ++l)
+    if (net->widths[l + 1] > 256) return fail(HRKAN_EUNSUPPORTED, "jet-spec engine: widths up to 256");
+  HR_CUDA(net->jets.ensure(sizeof(float) * (size_t)Pc * C * sumw));
+  HR_CUDA(net->adj_a.ensure(sizeof(float) * (size_t)Pc * C * maxw));
+  HR_CUDA(net->adj_b.ensure(sizeof(float) * (size_t)Pc * C * maxw));
+  HR_CUDA(net->loss_part.ensure(sizeof(float) * 2 * (size_t)((Pc + 255) / 256 + 1)));
+  HR_CUDA(net->w_part.ensure(sizeof(float) * (size_t)NZ_MAX * net->max_layer_w));
+  HR_CUDA(net->b_part.ensure(sizeof(float) * (size_t)NZ_MAX * net->max_width));
+  std::vector<float*> jet(L + 1, nullptr);
+  {
+    float* q = net->jets.f();
+    for (int l = 1; l <= L; ++l) {
+      jet[l] = q;
+      q += (size_t)Pc * C * net->widths[l];
+    }
+  }
+  const BasisCfg bc = net->bc;
+  JsPdeArgs pa{};
+  if (a.kind == PASS_INTERIOR) {
+    pa.alpha = a.pde->alpha;
+    pa.adv = a.pde->adv;
+    pa.disp3 = a.pde->disp3;
+    pa.disp5 = a.pde->disp5;
+    for (int q = 0; q < 6; ++q) pa.K[q] = a.pde->aniso[q];
+    pa.inv_n = a.inv_n;
+  }
+  for (int64_t c0 = 0; c0 < a.P; c0 += Pc) {
+    const int64_t n = std::min(Pc, a.P - c0);
+    const float* X0 = a.pts + c0 * D;
+    float* U = (a.kind == PASS_JET) ? a.jet_out + c0 * C : jet[L];
+    // ---------------- forward through every layer (a1, a2 on the generic jet)
+    for (int l = 0; l < L; ++l) {
+      const int I = net->widths[l], O = net->widths[l + 1];
+      const float* in = (l == 0) ? X0 : jet[l];
+      float* out = (l == L - 1) ? U : jet[l + 1];
+      const int cls = (l == 0) ? HRKAN_K_FWD_FIRST : (l == L - 1 ? HRKAN_K_FWD_LAST : HRKAN_K_FWD_HIDDEN);
+      if (O == 1) {
+        const unsigned g = (unsigned)((n + JS_LW - 1) / JS_LW);
+        if (l == 0) HR_LAUNCH(cls, "k_js_fwd_o1", (k_js_fwd_o1<S, M, true><<<g, 32 * JS_LW, 0, st>>>(in, net->params + net->w_off[l], net->params + net->b_off[l], out, n, I, bc)));
+        else HR_LAUNCH(cls, "k_js_fwd_o1", (k_js_fwd_o1<S, M, false><<<g, 32 * JS_LW, 0, st>>>(in, net->params + net->w_off[l], net->params + net->b_off[l], out, n, I, bc)));
+      } else {
+        const unsigned g = (unsigned)((n + JS_PT - 1) / JS_PT);
+        const int bd = (O + 31) / 32 * 32;
+        if (l == 0) HR_LAUNCH(cls, "k_js_fwd", (k_js_fwd<S, M, true><<<g, bd, 0, st>>>(in, net->wt[l], net->params + net->b_off[l], out, n, I, O, bc)));
+        else HR_LAUNCH(cls, "k_js_fwd", (k_js_fwd<S, M, false><<<g, bd, 0, st>>>(in, net->wt[l], net->params + net->b_off[l], out, n, I, O, bc)));
+      }
+    }
+    if (a.kind == PASS_JET) continue;
+    // ---------------- residual, loss and seeds (a3 on the generic jet)
+    float* ybar = net->adj_a.f();
+    float* xbar = net->adj_b.f();
+    const int nbl = (int)((n + 255) / 256);
+    if (a.pde->kind == HRKAN_KAWAHARA) {
+      if constexpr (C == 7) HR_LAUNCH(HRKAN_K_LOSS, "k_js_loss", (k_js_loss<S, JS_KAWAHARA><<<nbl, 256, 0, st>>>(U, a.forcing ? a.forcing + c0 : nullptr, ybar, net->loss_part.f(), n, pa)));
+      else return fail(HRKAN_EINVAL, "internal: Kawahara needs the Taylor-5 jet");
+    } else {
+      if constexpr (C != 7) HR_LAUNCH(HRKAN_K_LOSS, "k_js_loss", (k_js_loss<S, JS_ANISO><<<nbl, 256, 0, st>>>(U, a.forcing + c0, ybar, net->loss_part.f(), n, pa)));
+      else return fail(HRKAN_EINVAL, "internal: the anisotropic operator needs the Hessian jet");
+    }
+    HR_LAUNCH(HRKAN_K_REDUCE, "k_js_reduce_loss", (k_js_reduce_loss<<<1, 256, 0, st>>>(net->loss_part.f(), nbl, pa.alpha * pa.inv_n, a.out_loss, a.out_flag)));
+    // ---------------- reverse, last layer to first (a4-a7 on the generic jet)
+    for (int l = L - 1; l >= 0; --l) {
+      const int I = net->widths[l], O = net->widths[l + 1];
+      const float* in = (l == 0) ? X0 : jet[l];
+      float* dW = a.grad + net->w_off[l];
+      float* db = a.grad + net->b_off[l];
+      const int cls = (l == 0) ? HRKAN_K_WGRAD_FIRST : (l == L - 1 ? HRKAN_K_WGRAD_LAST : HRKAN_K_WGRAD_HIDDEN);
+      const int JW = (O == 1) ? 1 : 32;
+      const int IW = (O == 1) ? std::min(256, (I + 31) / 32 * 32) : 8;
+      const int gx = (O + JW - 1) / JW, gy = (I + IW - 1) / IW;
+      int nz = (int)std::max<int64_t>(1, (4 * net->num_sms + gx * gy - 1) / (gx * gy));
+      nz = (int)std::min<int64_t>(nz, std::max<int64_t>(1, n / 64));
+      nz = std::min(nz, NZ_MAX);
+      const size_t smem = sizeof(float) * (size_t)IW * net->B * JW;
+      if (smem > 200 * 1024) return fail(HRKAN_EUNSUPPORTED, "jet-spec wgrad tile exceeds shared memory");
+      auto wg = [&](auto kfn) -> hrkan_status {
+        HR_CUDA(smem_optin(kfn, smem));
+        HR_LAUNCH(cls, "k_js_wgrad", (kfn<<<dim3(gx, gy, nz), dim3(JW, IW), smem, st>>>(in, ybar, net->w_part.f(), net->b_part.f(), n, I, O, bc)));
+        return HRKAN_OK;
+      };
+      if (O == 1) {
+        if (l == 0) HR_TRY(wg(k_js_wgrad<S, M, true, 1>));
+        else HR_TRY(wg(k_js_wgrad<S, M, false, 1>));
+      } else {
+        if (l == 0) HR_TRY(wg(k_js_wgrad<S, M, true, 32>));
+        else HR_TRY(wg(k_js_wgrad<S, M, false, 32>));
+      }
+      const int64_t nW = (int64_t)O * I * net->B;
+      HR_LAUNCH(HRKAN_K_REDUCE, "k_reduce_parts",
+                k_reduce_parts<<<(unsigned)((nW + O + 255) / 256), 256, 0, st>>>(net->w_part.f(), net->b_part.f(), nz, nW, O, dW, db));
+      if (l > 0) {
+        const int64_t tot = n * I;
+        HR_LAUNCH(l == L - 1 ? HRKAN_K_DGRAD_LAST : HRKAN_K_DGRAD_HIDDEN, "k_js_dgrad",
+                  (k_js_dgrad<S, M><<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(in, net->params + net->w_off[l], ybar, xbar, n, I, O, bc)));
         std::swap(ybar, xbar);
       }
     }
@@ -271,5 +390,11 @@ hrkan_status run_tiny(hrkan_net* net, const TinyArgs& t, cudaStream_t st) {
   }                                                                                                \
   hrkan_status tiny_step_m##MM(hrkan_net* net, const TinyArgs& t, cudaStream_t st) {             \
     return run_tiny<MM>(net, t, st);                                                               \
+  }                                                                                                \
+  hrkan_status dispatch_spec_m##MM(hrkan_net* net, int spec, const PassArgs& a, cudaStream_t st) { \
+    if (spec == JSPEC_TAYLOR5) return run_pass_spec<JsTaylor5, MM>(net, a, st);                    \
+    if (spec == JSPEC_HESS2) return run_pass_spec<JsHess<2>, MM>(net, a, st);                      \
+    if (spec == JSPEC_HESS3) return run_pass_spec<JsHess<3>, MM>(net, a, st);                      \
+    return fail(HRKAN_EINVAL, "internal: unknown jet spec");                                       \
   }                                                                                                \
   }

@@ -262,17 +262,37 @@ __global__ void k_transpose_w(const float* __restrict__ W, float* __restrict__ W
 }
 
 // Bias-corrected Adam.  bc1 = 1 - beta1^t, bc2 = 1 - beta2^t.
+// Bias-corrected Adam.  The step count lives on the device (t_cnt[0] = t before this
+// step, t_cnt[1] = finished-block counter): every block computes the corrections for t + 1 and the
+// last block to finish advances t and resets the counter, so a CUDA-graph replay of this launch
+// keeps advancing the bias correction.
 __global__ void k_adam(float* __restrict__ theta, float* __restrict__ m, float* __restrict__ v,
                        const float* __restrict__ g, int64_t n, float lr, float b1, float b2, float eps,
-                       float inv_bc1, float inv_bc2) {
+                       int* __restrict__ t_cnt) {
+  __shared__ float s_bc[2];
+  if (threadIdx.x == 0) {
+    const double t = (double)(*(volatile int*)t_cnt + 1);
+    s_bc[0] = (float)(1.0 / (1.0 - pow((double)b1, t)));
+    s_bc[1] = (float)(1.0 / (1.0 - pow((double)b2, t)));
+  }
+  __syncthreads();
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (t >= n) return;
-  const float gi = g[t];
-  const float mi = fmaf(b1, m[t], (1.f - b1) * gi);
-  const float vi = fmaf(b2, v[t], (1.f - b2) * gi * gi);
-  m[t] = mi;
-  v[t] = vi;
-  theta[t] -= lr * (mi * inv_bc1) / (sqrtf(vi * inv_bc2) + eps);
+  if (t < n) {
+    const float gi = g[t];
+    const float mi = fmaf(b1, m[t], (1.f - b1) * gi);
+    const float vi = fmaf(b2, v[t], (1.f - b2) * gi * gi);
+    m[t] = mi;
+    v[t] = vi;
+    theta[t] -= lr * (mi * s_bc[0]) / (sqrtf(vi * s_bc[1]) + eps);
+  }
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(reinterpret_cast<unsigned*>(t_cnt + 1), 1u) == gridDim.x - 1) {
+      t_cnt[0] += 1;
+      t_cnt[1] = 0;
+      __threadfence();
+    }
+  }
 }
 
 // Counter-based Philox4x32-10 (Salmon et al., SC'11) + Box-Muller: W ~ N(0, std^2), b = 0.

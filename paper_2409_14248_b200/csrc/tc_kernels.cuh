@@ -597,7 +597,7 @@ hrkan_status tc_split_ybar(hrkan_net* net, int l, const float* Ybar, int64_t n, 
       constexpr int OO = decltype(OC)::value;
       auto kfn = k_split_ybar<C, OO>;
       constexpr int smem = 8 * C * (OO + 4) * 4;
-      if (smem > 48 * 1024) HR_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      HR_CUDA(smem_optin(kfn, smem));
       HR_LAUNCH(HRKAN_K_OTHER, "k_split_ybar",
                 kfn<<<(unsigned)nb8, 256, smem, st>>>(Ybar, n, (uint16_t*)net->tc_yw.p, (uint16_t*)net->tc_yd.p));
       return HRKAN_OK;

@@ -20,6 +20,9 @@ if os.environ.get("HRKAN_LIB"):             # experiment variants only (scripts/
 
 HRKAN_POISSON = 0
 HRKAN_BURGERS = 1
+HRKAN_KAWAHARA = 2
+HRKAN_ANISO = 3
+JET_TAYLOR5, JET_HESSIAN = 1, 2
 ENGINE_AUTO, ENGINE_SIMT, ENGINE_TC = 0, 1, 2
 
 KERNEL_CLASSES = ["fwd_first", "fwd_hidden", "fwd_last", "loss", "wgrad_first", "wgrad_hidden", "wgrad_last",
@@ -37,6 +40,7 @@ SYMBOLS = [
     ("hrkan_set_params", ctypes.c_int, [_P, _P, _P]),
     ("hrkan_init_params", ctypes.c_int, [_P, _U64, _P]),
     ("hrkan_forward_jet", ctypes.c_int, [_P, _P, _I64, _P, _P, _P, _P]),
+    ("hrkan_forward_jet_ex", ctypes.c_int, [_P, _I32, _P, _I64, _P, _P]),
     ("hrkan_pinn_loss_grad", ctypes.c_int, [_P, _P, _P, _P, _I64, _P, _P, _I64, _P, _P, _I64, _I64, _I64, _P, _P]),
     ("hrkan_adam_step", ctypes.c_int, [_P, _P, _F, _F, _F, _F, _P]),
     ("hrkan_set_chunk_points", ctypes.c_int, [_P, _I64]),
@@ -51,7 +55,8 @@ SYMBOLS = [
 
 
 class HrkanPde(ctypes.Structure):
-    _fields_ = [("kind", _I32), ("alpha", _F), ("adv", _F), ("visc", _F)]
+    _fields_ = [("kind", _I32), ("alpha", _F), ("adv", _F), ("visc", _F), ("disp3", _F), ("disp5", _F),
+                ("aniso", _F * 6)]
 
 
 class HrkanError(RuntimeError):
@@ -114,9 +119,20 @@ def _stream(stream) -> Optional[int]:
     return None
 
 
-def pde_struct(kind: str, alpha: float = 0.05, adv: float = 1.0, visc: float = 0.01 / math.pi) -> HrkanPde:
-    k = {"poisson": HRKAN_POISSON, "burgers": HRKAN_BURGERS}[kind]
-    return HrkanPde(k, alpha, adv if k == HRKAN_BURGERS else 0.0, visc if k == HRKAN_BURGERS else 0.0)
+def pde_struct(kind: str, alpha: float = 0.05, adv: float = 1.0, visc: float = 0.01 / math.pi,
+               disp3: float = 0.0, disp5: float = 0.0, aniso=None) -> HrkanPde:
+    """kind: "poisson" | "burgers" (adv, visc) | "kawahara" (adv, disp3, disp5) | "aniso" (aniso = the
+    upper-triangle coefficients of u_ab, D=2: xx, xy, yy; D=3: xx, xy, xz, yy, yz, zz)."""
+    k = {"poisson": HRKAN_POISSON, "burgers": HRKAN_BURGERS, "kawahara": HRKAN_KAWAHARA, "aniso": HRKAN_ANISO}[kind]
+    K = (_F * 6)(*(list(aniso or []) + [0.0] * (6 - len(aniso or []))))
+    return HrkanPde(k, alpha, adv if k in (HRKAN_BURGERS, HRKAN_KAWAHARA) else 0.0,
+                    visc if k == HRKAN_BURGERS else 0.0, disp3 if k == HRKAN_KAWAHARA else 0.0,
+                    disp5 if k == HRKAN_KAWAHARA else 0.0, K)
+
+
+def jet_channels(kind: int, D: int) -> int:
+    """Channels of hrkan_forward_jet_ex: TAYLOR5 [u, u_x .. u_xxxxx, u_t]; HESSIAN [u, u_a, u_ab (a <= b)]."""
+    return 7 if kind == JET_TAYLOR5 else 1 + D + D * (D + 1) // 2
 
 
 class HRKANNet:
@@ -201,6 +217,15 @@ class HRKANNet:
         _check(_lib.hrkan_forward_jet(self._h, _ptr(pts), P, _ptr(u), _ptr(du), _ptr(d2u), _stream(stream)),
                "hrkan_forward_jet")
         return u, du, d2u
+
+    def forward_jet_ex(self, kind: int, pts, jet=None, stream=None):
+        """Higher-order / mixed jet jet[P, C] (JET_TAYLOR5 or JET_HESSIAN, see include/hrkan.h)."""
+        import torch
+        P = _numel(pts) // self.D
+        if jet is None:
+            jet = torch.empty(P, jet_channels(kind, self.D), dtype=torch.float32, device=f"cuda:{self.device}")
+        _check(_lib.hrkan_forward_jet_ex(self._h, kind, _ptr(pts), P, _ptr(jet), _stream(stream)), "hrkan_forward_jet_ex")
+        return jet
 
     def pinn_loss_grad(self, pde: HrkanPde, interior, boundary, g_boundary, initial=None, g_initial=None,
                        forcing=None, n_int_global: Optional[int] = None, n_bi_global: Optional[int] = None,

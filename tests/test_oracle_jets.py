@@ -12,7 +12,6 @@ import hrkan_inputs as HI
 from oracle import hrkan_oracle as O2
 from oracle import hrkan_oracle_jets as OJ
 
-torch.set_default_dtype(torch.float64)
 
 
 def _sym_basis(m, s, e, xs):
@@ -31,7 +30,7 @@ def test_basis_all_orders_vs_sympy(m):
         en = sn + (k + 1) * h
         v = _sym_basis(m, sn, en, xs)
         pts = [sn + (en - sn) * sp.Rational(q, 17) for q in (1, 5, 8, 13, 16)]
-        xt = torch.tensor([float(p) for p in pts])
+        xt = torch.tensor([float(p) for p in pts], dtype=torch.float64)
         for d in range(9):
             got = OJ.basis(xt, s, e, m, d)[:, n].numpy()
             ref = np.array([float(sp.diff(v, xs, d).subs(xs, p)) for p in pts])
@@ -46,15 +45,15 @@ def test_basis_continuity_class(m):
     s, e = OJ.make_supports(5, 3, -1.0, 1.0)
     n = 4
     eps = 1e-7 * (e[n] - s[n])
-    x_in = torch.tensor([s[n] + eps, e[n] - eps])
-    x_out = torch.tensor([s[n] - eps, e[n] + eps, s[n], e[n]])
+    x_in = torch.tensor([s[n] + eps, e[n] - eps], dtype=torch.float64)
+    x_out = torch.tensor([s[n] - eps, e[n] + eps, s[n], e[n]], dtype=torch.float64)
     xs = sp.symbols("x")
     v = _sym_basis(m, sp.nsimplify(s[n]), sp.nsimplify(e[n]), xs)
     for d in range(m + 2):
         inside = OJ.basis(x_in, s, e, m, d)[:, n].numpy()
         assert np.all(OJ.basis(x_out, s, e, m, d)[:, n].numpy() == 0.0)
         lim = float(sp.diff(v, xs, d).subs(xs, sp.nsimplify(s[n])))
-        grid = torch.linspace(s[n], e[n], 401)[1:-1]
+        grid = torch.linspace(s[n], e[n], 401, dtype=torch.float64)[1:-1]
         scale = OJ.basis(grid, s, e, m, d)[:, n].abs().max().item()
         if d < m:
             assert lim == 0.0 and np.all(np.abs(inside) < 1e-4 * scale)
