@@ -347,6 +347,9 @@ __global__ void __launch_bounds__(FwdCfg<NF, NS, M, OO>::THREADS, 1)
   } else if (warp == TC_MMA_WARP) {
     // ===================== MMA issuer (one thread)
     if (lane == 0) {
+      // dbg bit 6: deliberate deadlock (the issuer waits for its own first commit) -- exercises the hang
+      // guard of debug builds (tests/test_gpu_hang_guard.py); never set in production
+      if (dbg & 64) tc::mbar_wait(&acc_full[0], 0);
       constexpr uint32_t idesc = tc::idesc_bf16(128, N);
       // counters and descriptors advance incrementally (no integer division per K-block)
       const uint32_t base = tc::smem_u32(smem);

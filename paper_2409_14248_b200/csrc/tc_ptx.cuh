@@ -35,8 +35,40 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
 #ifndef MBAR_SUSPEND_NS
 #define MBAR_SUSPEND_NS 0
 #endif
+// Hang guard (debug builds, -DHRKAN_HANG_GUARD=1): every wait is bounded by
+// HRKAN_HANG_CYCLES SM clock cycles (default 2^34, ~9 s at 1.9 GHz).  A wait that runs out prints the
+// block, thread, barrier and parity and executes a trap, so a barrier-phase bug surfaces as a launch
+// failure (HRKAN_ECUDA on the next call) instead of a hung GPU.  Production builds keep the unbounded
+// spin (no clock reads in the hot loops).
+#ifndef HRKAN_HANG_GUARD
+#define HRKAN_HANG_GUARD 0
+#endif
+#ifndef HRKAN_HANG_CYCLES
+#define HRKAN_HANG_CYCLES (1ll << 34)
+#endif
+__device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+static __device__ __noinline__ void hang_trap(uint64_t* bar, uint32_t parity) {
+  printf("hrkan hang guard: block (%d,%d,%d) thread %d waited > %lld cycles on mbarrier smem+0x%x parity %u\n",
+         (int)blockIdx.x, (int)blockIdx.y, (int)blockIdx.z, (int)threadIdx.x, (long long)HRKAN_HANG_CYCLES,
+         smem_u32(bar), parity);
+  __trap();
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-#if MBAR_SUSPEND_NS == 0
+#if HRKAN_HANG_GUARD
+  const long long t0 = clock64();
+  while (!mbar_try(bar, parity))
+    if (clock64() - t0 > (long long)HRKAN_HANG_CYCLES) hang_trap(bar, parity);
+#elif MBAR_SUSPEND_NS == 0
   asm volatile(
       "{\n\t.reg .pred p;\n"
       "WAIT_%=:\n\t"
