@@ -228,6 +228,9 @@ def loss_grad(net: Net, params, pde: dict, pts_int, pts_bi, g_bi, n_int_global=N
     lp, lb = loss_parts(net, pt, pde, pts_int, pts_bi, g_bi, n_int_global, n_bi_global, forcing)
     L = lp + lb
     flat = [t for pair in pt for t in pair]
+    if not L.requires_grad:                      # no points at all: L = 0, every gradient 0
+        return float(lp), float(lb), [(np.zeros_like(np.asarray(W, np.float64)), np.zeros_like(np.asarray(b, np.float64)))
+                                      for W, b in params]
     grads = torch.autograd.grad(L, flat, allow_unused=True)
     grads = [torch.zeros_like(t) if g is None else g for t, g in zip(flat, grads)]
     out = [(grads[2 * l].numpy(), grads[2 * l + 1].numpy()) for l in range(len(pt))]

@@ -42,6 +42,9 @@ constexpr int TC_GEN_THREADS = 128;   // one generator group (4 warps); the grou
 __host__ __device__ constexpr int tc_ngen(int C, int O) {
   return HRKAN_FWD_NGEN > 0 ? HRKAN_FWD_NGEN : (C == 1 || C == 4 || O <= 64) ? 4 : 3;
 }
+#ifndef HRKAN_FWD_SWAP
+#define HRKAN_FWD_SWAP 0          // 1: O = 64 forward with (channel, point) rows on the MMA M side (FwdCfg::SW; measured 12 % slower on C3, off)
+#endif
 constexpr int TC_WIN = 4;             // inputs per jet window (16-B TMA rows)
 constexpr int TC_NWIN = 8;            // jet-window ring depth
 
@@ -60,12 +63,18 @@ struct FwdCfg {
   static constexpr int NP = tc_np(C);
   static constexpr int N = NP * C;
   static constexpr int O = OO;                               // output neurons (64, 128 or 256)
-  static constexpr int NMT = (OO + 127) / 128;               // 128-row M-tiles
-  static constexpr int OP = 128 * NMT;                       // rows of the W tiles (zero-padded)
+  // O = 64 runs SWAPPED: M = 128 generated (channel, point) rows, two M-tiles over a 256-row operand,
+  // N = the 64 output neurons -- the MMA then costs 2 x 128x64 instead of a zero-padded 128 x N
+  // (tcgen05 issue floor max(M,128)*N/256 cycles: 64 vs 120 per K-step for C = 5)
+  static constexpr bool SW = HRKAN_FWD_SWAP && (OO == 64);
+  static constexpr int NROW = SW ? 256 : N;                  // rows of the generated operand buffer
+  static constexpr int NMT = SW ? 2 : (OO + 127) / 128;      // 128-row M-tiles (of W, or of the generated rows)
+  static constexpr int OP = SW ? 64 : 128 * NMT;             // rows of the W tiles (zero-padded when not swapped)
+  static constexpr int ACC_COLS = SW ? NMT * O : NMT * N;    // TMEM columns of one accumulator
   // bf16 operands, K-major, SWIZZLE_NONE: a K-block of 16 = 2 chunks of 8 elements (16 B per row).
   // Generated operand chunk stride padded to 64 B (mod 128 B): the generators' 8-B stores
   // (4 consecutive K of one row, chunk-fastest lanes) are bank-conflict free.
-  static constexpr int ACSB = N * 16 + 64;                   // chunk stride (bytes)
+  static constexpr int ACSB = NROW * 16 + 64;                // chunk stride (bytes)
   static constexpr int W_STAGE_BYTES = 2 * 2 * OP * 16;      // hi + lo, [2 chunks][OP rows][8] each
   static constexpr int A_STAGE_BYTES = 2 * 2 * ACSB;         // hi + lo, [2 chunks][N rows][8] each
   static constexpr int STAGE_BYTES = W_STAGE_BYTES + A_STAGE_BYTES;
@@ -75,13 +84,13 @@ struct FwdCfg {
   static constexpr int NSTAGE_FIT = (225 * 1024 - FIXED_BYTES) / STAGE_BYTES;   // static smem + margin
   static constexpr int NSTAGE = NSTAGE_FIT > 6 ? 6 : NSTAGE_FIT;
   static constexpr int SMEM_BYTES = NSTAGE * STAGE_BYTES + FIXED_BYTES;
-  static constexpr int NACC = (2 * NMT * N <= 512) ? 2 : 1;   // double-buffered accumulators if they fit
+  static constexpr int NACC = (2 * ACC_COLS <= 512) ? 2 : 1;  // double-buffered accumulators if they fit
   static constexpr int NGEN = tc_ngen(C, OO);
   static constexpr int MMA_WARP = 4 * NGEN, PROD_WARP = 4 * NGEN + 1, WIN_WARP = 4 * NGEN + 2;
   static constexpr int THREADS = 32 * (4 * NGEN + 3);        // + MMA warp + W producer warp + jet-window TMA warp
-  static constexpr uint32_t TMEM_COLS = tc_tmem_cols(NACC * NMT * N);
+  static constexpr uint32_t TMEM_COLS = tc_tmem_cols(NACC * ACC_COLS);
   static_assert(N % 16 == 0 && N <= 256, "bad N");
-  static_assert(NMT * N <= 512, "accumulators exceed TMEM");
+  static_assert(ACC_COLS <= 512, "accumulators exceed TMEM");
   static_assert(NSTAGE >= 2, "shared memory budget");
   static_assert(STAGE_BYTES % 128 == 0, "TMA windows after the stages need 128-B alignment");
   // groups write alternate K-blocks: a group's previous stage is NGEN back, so its lead over the oldest
@@ -172,6 +181,36 @@ __global__ void __launch_bounds__(FwdCfg<NF, NS, M, OO>::THREADS, 1)
       const int buf = sg % NACC;
       tc::mbar_wait(&acc_full[buf], (uint32_t)((sg / NACC) & 1));
       tc::tc_fence_after();
+      if constexpr (Cfg::SW) {
+        // swapped: TMEM lane = generated row (c, p) of M-tile t, columns = the 64 outputs; the
+        // (M-tile, 16-output chunk) units are shared round-robin by the generator groups
+#pragma unroll 1
+        for (int u = grp; u < NMT * (O / 16); u += TC_NGEN) {
+          const int t = u / (O / 16), o0 = (u % (O / 16)) * 16;
+          const int r = t * 128 + qw * 32 + lane;
+          const int c = r / NP, pl = r - (r / NP) * NP;
+          const int64_t p = p0 + pl;
+          const bool ok = r < N && p < P;
+          float v[16];
+          tc::tmem_ld16(tmem + ((uint32_t)(qw * 32) << 16) + (uint32_t)((buf * NMT + t) * O + o0), v);
+          float4* yp = reinterpret_cast<float4*>(Y + (p * C + c) * (int64_t)O + o0);
+          if (ok) {
+            if (sg == 0 && c == 0) {
+#pragma unroll
+              for (int q = 0; q < 16; ++q) v[q] += __ldg(bias + o0 + q);
+            }
+            if (sg > 0) {
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const float4 old = yp[q];
+                v[4 * q] += old.x; v[4 * q + 1] += old.y; v[4 * q + 2] += old.z; v[4 * q + 3] += old.w;
+              }
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) yp[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+          }
+        }
+      } else {
 #pragma unroll 1
       for (int t = 0; t < NMT; ++t) {
         const int o = t * 128 + qw * 32 + lane;
@@ -205,6 +244,7 @@ __global__ void __launch_bounds__(FwdCfg<NF, NS, M, OO>::THREADS, 1)
           for (int q = 0; q < 16; ++q)
             if (ok[q]) *yp[q] = v[q];
         }
+      }
       }
       tc::tc_fence_before();
       tc::mbar_arrive(&acc_empty[buf]);
@@ -350,7 +390,7 @@ __global__ void __launch_bounds__(FwdCfg<NF, NS, M, OO>::THREADS, 1)
       // dbg bit 6: deliberate deadlock (the issuer waits for its own first commit) -- exercises the hang
       // guard of debug builds (tests/test_gpu_hang_guard.py); never set in production
       if (dbg & 64) tc::mbar_wait(&acc_full[0], 0);
-      constexpr uint32_t idesc = tc::idesc_bf16(128, N);
+      constexpr uint32_t idesc = Cfg::SW ? tc::idesc_bf16(128, O) : tc::idesc_bf16(128, N);
       // counters and descriptors advance incrementally (no integer division per K-block)
       const uint32_t base = tc::smem_u32(smem);
       const uint64_t bh0 = tc::smem_desc(base + Cfg::W_STAGE_BYTES, ACSB, 128);
@@ -371,10 +411,17 @@ __global__ void __launch_bounds__(FwdCfg<NF, NS, M, OO>::THREADS, 1)
 #pragma unroll
         for (int t = 0; t < NMT; ++t) {
           const uint64_t toff = off + (uint64_t)((t * 128 * 16) >> 4);
-          const uint32_t d = tmem + (uint32_t)((buf * NMT + t) * N);
-          tc::mma_bf16(d, wl0 + toff, bh0 + off, idesc, seg_first ? 0u : 1u);
-          tc::mma_bf16(d, wh0 + toff, bl0 + off, idesc, 1u);
-          tc::mma_bf16(d, wh0 + toff, bh0 + off, idesc, 1u);
+          if constexpr (Cfg::SW) {            // A = generated rows of M-tile t, B = W (64 rows)
+            const uint32_t d = tmem + (uint32_t)((buf * NMT + t) * O);
+            tc::mma_bf16(d, bl0 + toff, wh0 + off, idesc, seg_first ? 0u : 1u);
+            tc::mma_bf16(d, bh0 + toff, wl0 + off, idesc, 1u);
+            tc::mma_bf16(d, bh0 + toff, wh0 + off, idesc, 1u);
+          } else {
+            const uint32_t d = tmem + (uint32_t)((buf * NMT + t) * N);
+            tc::mma_bf16(d, wl0 + toff, bh0 + off, idesc, seg_first ? 0u : 1u);
+            tc::mma_bf16(d, wh0 + toff, bl0 + off, idesc, 1u);
+            tc::mma_bf16(d, wh0 + toff, bh0 + off, idesc, 1u);
+          }
         }
         tc::mma_commit(&empty_bar[s]);
         if (++segc == seg || kb == nkb - 1) {
@@ -518,7 +565,7 @@ hrkan_status tc_refresh_weights(hrkan_net* net, cudaStream_t st) {
     TcLayerState& ls = net->tc_layers[l];
     const int K = I * net->B;
     ls.nkb = (K + TC_KB - 1) / TC_KB;
-    const int OP = (O + 127) / 128 * 128;
+    const int OP = (HRKAN_FWD_SWAP && O == 64) ? 64 : (O + 127) / 128 * 128;   // FwdCfg::OP (O = 64 runs swapped)
     const size_t n = (size_t)ls.nkb * 2 * OP * TC_KB;
     if (!ls.w_fwd) {
       if (cudaMalloc(&ls.w_fwd, n * sizeof(uint16_t)) != cudaSuccess) return fail(HRKAN_ENOMEM, "tc weight alloc");
