@@ -14,6 +14,9 @@
 // runs t+1.  Epilogue: TMEM -> smem slice of SLICE_P points -> each (point, input) gathers only the
 // k+1 non-zero bases of its x (input jets TMA-loaded per M-tile) -> Xbar[p][c][i].
 #pragma once
+#ifndef HRKAN_DGR_NSTAGE_MAX
+#define HRKAN_DGR_NSTAGE_MAX 8   // stage-ring depth cap (shared memory permitting)
+#endif
 
 namespace {
 
@@ -72,7 +75,7 @@ struct DgrCfg {
   static constexpr int S_FLOATS = SLICE_P * C * DGR_SST;
   static constexpr int FIXED_BYTES = 4 * (2 * JET_FLOATS + S_FLOATS + 2 * NP * C) + 1024;   // + split-input carries
   static constexpr int NSTAGE_FIT = (225 * 1024 - FIXED_BYTES) / STAGE_BYTES;
-  static constexpr int NSTAGE = NSTAGE_FIT > 8 ? 8 : NSTAGE_FIT;
+  static constexpr int NSTAGE = NSTAGE_FIT > HRKAN_DGR_NSTAGE_MAX ? HRKAN_DGR_NSTAGE_MAX : NSTAGE_FIT;
   static constexpr int SMEM_BYTES = NSTAGE * STAGE_BYTES + FIXED_BYTES;
   static constexpr uint32_t TMEM_COLS = tc_tmem_cols(2 * N);
   static constexpr int EPI_WARPS = dgr_epi_warps(C);           // multiple of 4 (TMEM lane quadrants)
@@ -321,7 +324,7 @@ __global__ void __launch_bounds__(DgrCfg<NF, NS, M, OO>::THREADS, 1)
       if (lane == 0) tc::mbar_arrive(&jet_empty[buf]);
     }
   } else if (warp == DGR_MMA_WARP) {
-    if (lane == 0) {
+    {   // the whole warp runs the issue loop, one elected lane issues (tc::mma_bf16_w)
       constexpr uint32_t idesc = tc::idesc_bf16(128, N);
       for (int mt = 0; mt < nmt; ++mt) {
         const int buf = mt & 1;
@@ -342,12 +345,12 @@ __global__ void __launch_bounds__(DgrCfg<NF, NS, M, OO>::THREADS, 1)
           const uint64_t yh = tc::smem_desc(y_hi, N * 16, 128);
           const uint64_t yl = tc::smem_desc(y_lo, N * 16, 128);
           const uint32_t d = tmem + (uint32_t)(buf * N);
-          tc::mma_bf16(d, wl, yh, idesc, kb > 0 ? 1u : 0u);
-          tc::mma_bf16(d, wh, yl, idesc, 1u);
-          tc::mma_bf16(d, wh, yh, idesc, 1u);
-          tc::mma_commit(&empty_bar[s]);
+          tc::mma_bf16_w(d, wl, yh, idesc, kb > 0 ? 1u : 0u);
+          tc::mma_bf16_w(d, wh, yl, idesc, 1u);
+          tc::mma_bf16_w(d, wh, yh, idesc, 1u);
+          tc::mma_commit_w(&empty_bar[s]);
         }
-        tc::mma_commit(&acc_full[buf]);
+        tc::mma_commit_w(&acc_full[buf]);
       }
     }
     __syncwarp();

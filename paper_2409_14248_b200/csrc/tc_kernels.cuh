@@ -20,6 +20,9 @@
 //   TMEM segments (+bias -> Y[p][c][o], coalesced); then the MMA warp (TMEM allocator + single-thread
 //   tcgen05.mma issuer), the W bulk-copy warp and the jet-window TMA warp (FwdCfg::*_WARP).
 #pragma once
+#ifndef HRKAN_FWD_NSTAGE_MAX
+#define HRKAN_FWD_NSTAGE_MAX 6   // stage-ring depth cap (shared memory permitting)
+#endif
 #include "tc_ptx.cuh"
 
 namespace {
@@ -82,7 +85,7 @@ struct FwdCfg {
   static constexpr int WIN_FLOATS = NP * CB * TC_WIN;        // TMA box [NP points][CB][TC_WIN inputs]
   static constexpr int FIXED_BYTES = 4 * TC_NWIN * WIN_FLOATS + 2 * 4 * 256 + 1024;   // windows, ctr, -ctr*sc
   static constexpr int NSTAGE_FIT = (225 * 1024 - FIXED_BYTES) / STAGE_BYTES;   // static smem + margin
-  static constexpr int NSTAGE = NSTAGE_FIT > 6 ? 6 : NSTAGE_FIT;
+  static constexpr int NSTAGE = NSTAGE_FIT > HRKAN_FWD_NSTAGE_MAX ? HRKAN_FWD_NSTAGE_MAX : NSTAGE_FIT;
   static constexpr int SMEM_BYTES = NSTAGE * STAGE_BYTES + FIXED_BYTES;
   static constexpr int NACC = (2 * ACC_COLS <= 512) ? 2 : 1;  // double-buffered accumulators if they fit
   static constexpr int NGEN = tc_ngen(C, OO);
@@ -385,8 +388,8 @@ __global__ void __launch_bounds__(FwdCfg<NF, NS, M, OO>::THREADS, 1)
     }
     while (next_drain < nseg) drain(next_drain++);
   } else if (warp == TC_MMA_WARP) {
-    // ===================== MMA issuer (one thread)
-    if (lane == 0) {
+    // ===================== MMA issuer: the whole warp runs the loop, one elected lane issues (tc::mma_bf16_w)
+    {
       // dbg bit 6: deliberate deadlock (the issuer waits for its own first commit) -- exercises the hang
       // guard of debug builds (tests/test_gpu_hang_guard.py); never set in production
       if (dbg & 64) tc::mbar_wait(&acc_full[0], 0);
@@ -398,11 +401,11 @@ __global__ void __launch_bounds__(FwdCfg<NF, NS, M, OO>::THREADS, 1)
       const uint64_t wh0 = tc::smem_desc(base, OP * 16, 128);
       const uint64_t wl0 = tc::smem_desc(base + 2 * OP * 16, OP * 16, 128);
       int s = 0, segc = 0, buf = 0, sgi = 0;
-      uint32_t ph = 0, use[2] = {0u, 0u};
+      uint32_t ph = 0, use0 = 0u, use1 = 0u;
       for (int kb = 0; kb < nkb; ++kb) {
         const bool seg_first = segc == 0;
         if (seg_first && sgi >= NACC) {
-          tc::mbar_wait(&acc_empty[buf], (use[buf] - 1) & 1);
+          tc::mbar_wait(&acc_empty[buf], ((buf ? use1 : use0) - 1) & 1);
           tc::tc_fence_after();
         }
         tc::mbar_wait(&full_bar[s], ph);
@@ -413,21 +416,21 @@ __global__ void __launch_bounds__(FwdCfg<NF, NS, M, OO>::THREADS, 1)
           const uint64_t toff = off + (uint64_t)((t * 128 * 16) >> 4);
           if constexpr (Cfg::SW) {            // A = generated rows of M-tile t, B = W (64 rows)
             const uint32_t d = tmem + (uint32_t)((buf * NMT + t) * O);
-            tc::mma_bf16(d, bl0 + toff, wh0 + off, idesc, seg_first ? 0u : 1u);
-            tc::mma_bf16(d, bh0 + toff, wl0 + off, idesc, 1u);
-            tc::mma_bf16(d, bh0 + toff, wh0 + off, idesc, 1u);
+            tc::mma_bf16_w(d, bl0 + toff, wh0 + off, idesc, seg_first ? 0u : 1u);
+            tc::mma_bf16_w(d, bh0 + toff, wl0 + off, idesc, 1u);
+            tc::mma_bf16_w(d, bh0 + toff, wh0 + off, idesc, 1u);
           } else {
             const uint32_t d = tmem + (uint32_t)((buf * NMT + t) * N);
-            tc::mma_bf16(d, wl0 + toff, bh0 + off, idesc, seg_first ? 0u : 1u);
-            tc::mma_bf16(d, wh0 + toff, bl0 + off, idesc, 1u);
-            tc::mma_bf16(d, wh0 + toff, bh0 + off, idesc, 1u);
+            tc::mma_bf16_w(d, wl0 + toff, bh0 + off, idesc, seg_first ? 0u : 1u);
+            tc::mma_bf16_w(d, wh0 + toff, bl0 + off, idesc, 1u);
+            tc::mma_bf16_w(d, wh0 + toff, bh0 + off, idesc, 1u);
           }
         }
-        tc::mma_commit(&empty_bar[s]);
+        tc::mma_commit_w(&empty_bar[s]);
         if (++segc == seg || kb == nkb - 1) {
-          tc::mma_commit(&acc_full[buf]);
+          tc::mma_commit_w(&acc_full[buf]);
           segc = 0;
-          ++use[buf];
+          if (buf) ++use1; else ++use0;
           ++sgi;
           if (NACC == 2) buf ^= 1;
         }

@@ -18,7 +18,10 @@ CLASS = [("k_fwd_first", "fwd_first"), ("k_fwd_tc", "fwd_hidden"), ("k_fwd_simt"
 
 def main():
     rep, cfg, npts, out = sys.argv[1], sys.argv[2], int(sys.argv[3]), sys.argv[4]
-    txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    if rep.endswith(".csv"):                  # an exported `--page raw --csv` of the report
+        txt = open(rep).read()
+    else:
+        txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(txt)))
     hdr = rows[0]
     ix = {h: i for i, h in enumerate(hdr)}
@@ -48,7 +51,11 @@ def main():
         t_unit = rows[1][ix["gpu__time_duration.sum"]]
         t = val(r, "gpu__time_duration.sum")
         t_ms = t / 1e6 if t_unit == "ns" else t / 1e3 if t_unit in ("us", "usecond") else t
-        entry = {"class": cls, "time_ms": t_ms,
+        stalls = {h.replace("smsp__pcsamp_warps_issue_stalled_", ""): val(r, h) or 0.0 for h in hdr
+                  if h.startswith("smsp__pcsamp_warps_issue_stalled_") and not h.endswith("not_issued")}
+        tot = sum(stalls.values()) or 1.0
+        top = sorted(stalls.items(), key=lambda kv: -kv[1])[:3]
+        entry = {"class": cls, "time_ms": t_ms, "top_stalls": {k: round(100 * v / tot, 1) for k, v in top},
                  "tensor_pipe_pct": val(r, "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed") or 0.0,
                  "issue_active_pct": val(r, "smsp__issue_active.avg.pct_of_peak_sustained_active"),
                  "lts_pct": val(r, "lts__t_sectors.avg.pct_of_peak_sustained_elapsed"),
@@ -63,12 +70,14 @@ def main():
           "points_per_capture": npts, "kernels": kernels}
     json.dump(js, open(out + ".json", "w"), indent=1)
     lines = [f"# ncu summary, {cfg} (interior pass, {npts} points; `ncu --set full --clock-control none`)", "",
-             "| kernel | time ms | tensor pipe % | issue % | L2 % | DRAM B/point | SM GHz |", "|---|---|---|---|---|---|---|"]
+             "| kernel | time ms | tensor pipe % | issue % | L2 % | DRAM B/point | SM GHz | top stall reasons (% of samples) |",
+             "|---|---|---|---|---|---|---|---|"]
     for k, e in sorted(kernels.items(), key=lambda kv: -kv[1]["time_ms"]):
         if e["time_ms"] < 0.005:
             continue
         lines.append(f"| `{k}` | {e['time_ms']:.3f} | {e['tensor_pipe_pct']:.1f} | {e['issue_active_pct'] or 0:.1f} | "
-                     f"{e['lts_pct'] or 0:.1f} | {e['dram_bytes_per_point']:.0f} | {e['sm_clock_ghz'] or 0:.2f} |")
+                     f"{e['lts_pct'] or 0:.1f} | {e['dram_bytes_per_point']:.0f} | {e['sm_clock_ghz'] or 0:.2f} | "
+                     + ", ".join(f"{k} {v}" for k, v in e.get("top_stalls", {}).items()) + " |")
     open(out + "_summary.md", "w").write("\n".join(lines) + "\n")
     print("\n".join(lines))
 
