@@ -129,8 +129,12 @@ __global__ void __launch_bounds__(DgrCfg<NF, NS, M, OO>::THREADS, 1)
   __shared__ __align__(8) uint64_t jet_full[2], jet_empty[2];
   __shared__ uint32_t tmem_base_sh;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t p0 = (int64_t)blockIdx.x * NP;
-  const int nblk = nmt * NKB;
+  // persistent (one CTA per SM): point tiles blockIdx.x + jt*gridDim.x, each run as nmt M-tiles; the
+  // global M-tile counter gm = jt*nmt + mt drives the accumulator / jet-box / carry double buffers and
+  // g = gm*NKB + kb the stage ring, so tile jt+1's MMAs overlap tile jt's epilogue
+  const int64_t ntiles = (P + NP - 1) / NP;
+  const int ntl = (int)((ntiles - (int64_t)blockIdx.x + gridDim.x - 1) / gridDim.x);
+  const int nmt_tot = ntl * nmt;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < NSTAGE; ++s) {
@@ -157,11 +161,14 @@ __global__ void __launch_bounds__(DgrCfg<NF, NS, M, OO>::THREADS, 1)
     const int half = warp >> 2;                   // which of the NH column phases this warp drains
     const int etid = threadIdx.x;
     const int r = qw * 32 + lane;                 // accumulator row = il*B + n
-    for (int mt = 0; mt < nmt; ++mt) {
-      const int buf = mt & 1;
-      tc::mbar_wait(&acc_full[buf], (uint32_t)((mt >> 1) & 1));
+#pragma unroll 1
+    for (int gm = 0; gm < nmt_tot; ++gm) {
+      const int jt = gm / nmt, mt = gm - jt * nmt;
+      const int64_t p0 = ((int64_t)blockIdx.x + (int64_t)jt * gridDim.x) * NP;
+      const int buf = gm & 1;
+      tc::mbar_wait(&acc_full[buf], (uint32_t)((gm >> 1) & 1));
       tc::tc_fence_after();
-      tc::mbar_wait(&jet_full[buf], (uint32_t)((mt >> 1) & 1));
+      tc::mbar_wait(&jet_full[buf], (uint32_t)((gm >> 1) & 1));
       const int B = bc.B;
       const int row0 = mt * RPT, nrows = min(RPT, I * B - row0);   // this tile's K rows
       const int i_first = row0 / B, n_in = (row0 + nrows - 1) / B - i_first + 1;
@@ -295,14 +302,14 @@ __global__ void __launch_bounds__(DgrCfg<NF, NS, M, OO>::THREADS, 1)
 #endif
           // carries alternate by tile parity: a tile reads its predecessor's and writes its own
           if (n_lo > 0) {                          // input started in the previous tile: add its part
-            const float* cp = carry + (((mt + 1) & 1) * NP + pl) * C;
+            const float* cp = carry + (((gm + 1) & 1) * NP + pl) * C;
             xb += cp[0];
 #pragma unroll
             for (int a = 0; a < NF; ++a) dxb[a] += cp[1 + a];
 #pragma unroll
             for (int a = 0; a < NS; ++a) ddxb[a] += cp[1 + NF + a];
           }
-          float* cp = carry + ((mt & 1) * NP + pl) * C;
+          float* cp = carry + ((gm & 1) * NP + pl) * C;
           if (n_hi < B) {                          // input continues in the next tile: carry the part
             cp[0] = xb;
 #pragma unroll
@@ -326,15 +333,18 @@ __global__ void __launch_bounds__(DgrCfg<NF, NS, M, OO>::THREADS, 1)
   } else if (warp == DGR_MMA_WARP) {
     {   // the whole warp runs the issue loop, one elected lane issues (tc::mma_bf16_w)
       constexpr uint32_t idesc = tc::idesc_bf16(128, N);
-      for (int mt = 0; mt < nmt; ++mt) {
-        const int buf = mt & 1;
-        if (mt >= 2) {
-          tc::mbar_wait(&acc_empty[buf], (uint32_t)(((mt >> 1) - 1) & 1));
+      int s = 0;
+      uint32_t ph = 0;
+#pragma unroll 1
+      for (int gm = 0; gm < nmt_tot; ++gm) {
+        const int buf = gm & 1;
+        if (gm >= 2) {
+          tc::mbar_wait(&acc_empty[buf], (uint32_t)(((gm >> 1) - 1) & 1));
           tc::tc_fence_after();
         }
+#pragma unroll 1
         for (int kb = 0; kb < NKB; ++kb) {
-          const int g = mt * NKB + kb, s = g % NSTAGE;
-          tc::mbar_wait(&full_bar[s], (g / NSTAGE) & 1);
+          tc::mbar_wait(&full_bar[s], ph);
           tc::tc_fence_after();
           const uint32_t w_hi = tc::smem_u32(smem + s * Cfg::STAGE_BYTES);
           const uint32_t w_lo = w_hi + 2 * 128 * 16;
@@ -349,6 +359,7 @@ __global__ void __launch_bounds__(DgrCfg<NF, NS, M, OO>::THREADS, 1)
           tc::mma_bf16_w(d, wh, yl, idesc, 1u);
           tc::mma_bf16_w(d, wh, yh, idesc, 1u);
           tc::mma_commit_w(&empty_bar[s]);
+          if (++s == NSTAGE) { s = 0; ph ^= 1u; }
         }
         tc::mma_commit_w(&acc_full[buf]);
       }
@@ -358,21 +369,20 @@ __global__ void __launch_bounds__(DgrCfg<NF, NS, M, OO>::THREADS, 1)
     // ===================== producer: W^T and pre-split Ybar stages (1-D bulk copies); never waits on the
     // epilogue, so the MMA is only held back by the TMEM accumulators it releases early
     if (lane == 0) {
-      const uint16_t* ytile = Ysplit + (int64_t)blockIdx.x * NKB * (Cfg::Y_STAGE_BYTES / 2);
-#ifndef HRKAN_DGR_PREFETCH
-#define HRKAN_DGR_PREFETCH 0
-#endif
-      for (int g = 0; g < nblk; ++g) {
-        const int kb = g - (g / NKB) * NKB;
-        const int s = g % NSTAGE;
-        if (HRKAN_DGR_PREFETCH > 0 && g + HRKAN_DGR_PREFETCH < NKB)   // first M-tile pass streams Ybar from HBM
-          tc::bulk_prefetch_l2(ytile + (int64_t)(g + HRKAN_DGR_PREFETCH) * (Cfg::Y_STAGE_BYTES / 2), Cfg::Y_STAGE_BYTES);
-        tc::mbar_wait(&empty_bar[s], ((g / NSTAGE) & 1) ^ 1);
-        tc::mbar_arrive_expect_tx(&full_bar[s], Cfg::STAGE_BYTES);
-        tc::bulk_g2s(smem + s * Cfg::STAGE_BYTES, Wtiled + (int64_t)g * (Cfg::W_STAGE_BYTES / 2), Cfg::W_STAGE_BYTES,
-                     &full_bar[s]);
-        tc::bulk_g2s(smem + s * Cfg::STAGE_BYTES + Cfg::W_STAGE_BYTES, ytile + (int64_t)kb * (Cfg::Y_STAGE_BYTES / 2),
-                     Cfg::Y_STAGE_BYTES, &full_bar[s]);
+      int s = 0;
+      uint32_t ph = 0;
+      for (int jt = 0; jt < ntl; ++jt) {
+        const uint16_t* ytile = Ysplit + ((int64_t)blockIdx.x + (int64_t)jt * gridDim.x) * NKB * (Cfg::Y_STAGE_BYTES / 2);
+        for (int g = 0; g < nmt * NKB; ++g) {       // W^T stage g = mt*NKB + kb of this point tile
+          const int kb = g - (g / NKB) * NKB;
+          tc::mbar_wait(&empty_bar[s], ph ^ 1u);
+          tc::mbar_arrive_expect_tx(&full_bar[s], Cfg::STAGE_BYTES);
+          tc::bulk_g2s(smem + s * Cfg::STAGE_BYTES, Wtiled + (int64_t)g * (Cfg::W_STAGE_BYTES / 2), Cfg::W_STAGE_BYTES,
+                       &full_bar[s]);
+          tc::bulk_g2s(smem + s * Cfg::STAGE_BYTES + Cfg::W_STAGE_BYTES, ytile + (int64_t)kb * (Cfg::Y_STAGE_BYTES / 2),
+                       Cfg::Y_STAGE_BYTES, &full_bar[s]);
+          if (++s == NSTAGE) { s = 0; ph ^= 1u; }
+        }
       }
     }
     __syncwarp();
@@ -380,11 +390,13 @@ __global__ void __launch_bounds__(DgrCfg<NF, NS, M, OO>::THREADS, 1)
     // ===================== jet producer: input-jet boxes of the M-tiles (TMA), two tiles ahead of use
     if (lane == 0) {
       tc::tma_prefetch_desc(&tmX);
-      for (int mt = 0; mt < nmt; ++mt) {
-        const int jb = mt & 1;
-        if (mt >= 2) tc::mbar_wait(&jet_empty[jb], (uint32_t)(((mt >> 1) - 1) & 1));
+      for (int gm = 0; gm < nmt_tot; ++gm) {
+        const int jt = gm / nmt, mt = gm - jt * nmt;
+        const int p0 = (int)(((int64_t)blockIdx.x + (int64_t)jt * gridDim.x) * NP);
+        const int jb = gm & 1;
+        if (gm >= 2) tc::mbar_wait(&jet_empty[jb], (uint32_t)(((gm >> 1) - 1) & 1));
         tc::mbar_arrive_expect_tx(&jet_full[jb], Cfg::JET_FLOATS * 4);
-        tc::tma_load_3d(jets + jb * Cfg::JET_FLOATS, &tmX, ((mt * RPT) / bc.B) & ~3, 0, (int)p0, &jet_full[jb]);
+        tc::tma_load_3d(jets + jb * Cfg::JET_FLOATS, &tmX, ((mt * RPT) / bc.B) & ~3, 0, p0, &jet_full[jb]);
       }
     }
     __syncwarp();

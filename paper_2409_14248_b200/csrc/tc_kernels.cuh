@@ -737,7 +737,8 @@ hrkan_status launch_dgrad_tc(hrkan_net* net, int l, const float* X, const float*
   const int I = net->widths[l];
   CUtensorMap tmX;
   HR_TRY(make_tmap_f32_3d(&tmX, X, (uint64_t)I, (uint64_t)Cfg::C, (uint64_t)n, DGR_IPTB, Cfg::C, Cfg::NP));
-  const unsigned grid = (unsigned)((n + Cfg::NP - 1) / Cfg::NP);
+  const int64_t ntiles = (n + Cfg::NP - 1) / Cfg::NP;
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ntiles, net->num_sms));   // persistent
   HR_LAUNCH(HRKAN_K_DGRAD_HIDDEN, "k_dgrad_tc",
             kfn<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, st>>>(tmX, (const uint16_t*)net->tc_yd.p, ls.w_dgr, Xbar, n, I,
                                                             dgr_rows_per_tile(net->B, net->D), ls.ntile_dgr, net->bc,
