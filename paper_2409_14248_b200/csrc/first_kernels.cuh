@@ -134,6 +134,85 @@ __global__ void __launch_bounds__(FL_THREADS) k_fwd_first(const float* __restric
   }
 }
 
+// Forward of the first layer for interior passes (NF > 0), W staged in shared memory.
+// Ws[a][KT + n][o] (n in [-KT, B + KT)) holds W^T with KT zero rows on each side, and the per-batch table
+// stores the clamped first basis n0 and the values of the KT candidate bases n0 .. n0+KT-1 (zero outside
+// the support, beyond k and outside [0, B)), so the contraction is KT unpredicated shared loads of W and
+// 3*KT FFMAs per (point, coordinate, output) -- no global loads and no branches in the inner loop.
+// Persistent grid (blocks stride over the 32-point batches).  KT = 4 covers k <= 3, KT = 8 any k <= 7.
+template <int KT>
+struct __align__(16) FlTab {
+  float v[3][KT];       // v, v', v'' of the candidate bases n0 .. n0+KT-1
+  int n0;               // clamped to [-KT, B]
+  int pad[3];
+};
+
+template <int NF, int NS, int M, int KT>
+__global__ void __launch_bounds__(FL_THREADS) k_fwd_first_s(const float* __restrict__ pts, const float* __restrict__ Wt,
+                                                            const float* __restrict__ bias, float* __restrict__ Y,
+                                                            int64_t P, int O, BasisCfg bc) {
+  constexpr int D = NF;
+  constexpr int C = 1 + NF + NS;
+  extern __shared__ __align__(16) float fsm[];
+  FlTab<KT>* tab = reinterpret_cast<FlTab<KT>*>(fsm);          // [FL_BATCH][D]
+  float* Ws = fsm + FL_BATCH * D * (int)(sizeof(FlTab<KT>) / 4);   // [D][B + 2 KT][O]
+  const int B = bc.B, BP = B + 2 * KT;
+  for (int e = threadIdx.x; e < D * BP * O; e += blockDim.x) {
+    const int o = e % O, r = e / O, a = r / BP, n = r - a * BP - KT;
+    Ws[e] = (n >= 0 && n < B) ? __ldg(Wt + ((int64_t)a * B + n) * O + o) : 0.f;
+  }
+  const int QG = (int)blockDim.x / O;                            // point groups (O <= blockDim)
+  const int qg = (int)threadIdx.x / O, o = (int)threadIdx.x % O;
+  const float b = (qg < QG) ? __ldg(bias + o) : 0.f;
+  for (int64_t p0 = (int64_t)blockIdx.x * FL_BATCH; p0 < P; p0 += (int64_t)gridDim.x * FL_BATCH) {
+    __syncthreads();                                             // Ws staged / previous batch consumed
+    for (int e = threadIdx.x; e < FL_BATCH * D; e += blockDim.x) {
+      const int q = e / D, a = e - (e / D) * D;
+      const int64_t p = p0 + q;
+      const float x = (p < P) ? __ldg(pts + p * D + a) : 0.f;
+      const int n0 = first_basis(x, bc);
+      FlTab<KT>& t = tab[q * D + a];
+#pragma unroll
+      for (int r = 0; r < KT; ++r) {
+        const int n = n0 + r;
+        float v0 = 0.f, v1 = 0.f, v2 = 0.f, v3;
+        if (r <= bc.k && n >= 0 && n < B) hr_eval<M, (NS > 0 ? 2 : 1)>(basis_q(x, n, bc), bc.sc, v0, v1, v2, v3);
+        t.v[0][r] = (r == 0 && x != x) ? x : v0;   // propagate NaN inputs (the support test would drop them)
+        t.v[1][r] = v1;
+        t.v[2][r] = v2;
+      }
+      t.n0 = (x != x) ? 0 : min(max(n0, -KT), B);
+    }
+    __syncthreads();
+    if (qg >= QG) continue;
+    const int nq = (int)((P - p0) < FL_BATCH ? (P - p0) : FL_BATCH);
+#pragma unroll 2
+    for (int q = qg; q < nq; q += QG) {
+      float acc[C];
+      acc[0] = b;
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        const FlTab<KT>& t = tab[q * D + a];
+        const float* wp = Ws + (a * BP + KT + t.n0) * O + o;
+        float s0 = 0.f, s1 = 0.f, s2 = 0.f;
+#pragma unroll
+        for (int r = 0; r < KT; ++r) {
+          const float w = wp[r * O];
+          s0 = fmaf(w, t.v[0][r], s0);
+          s1 = fmaf(w, t.v[1][r], s1);
+          s2 = fmaf(w, t.v[2][r], s2);
+        }
+        acc[0] += s0;
+        acc[1 + a] = s1;
+        if (a < NS) acc[1 + NF + a] = s2;
+      }
+      float* out = Y + (p0 + q) * (int64_t)(C * O) + o;
+#pragma unroll
+      for (int c = 0; c < C; ++c) out[c * O] = acc[c];
+    }
+  }
+}
+
 // Weight gradient of the first layer: a grid of blocks over contiguous point ranges; thread (o, point
 // group qg) keeps its (a, n) accumulators in shared memory acc[qg][a][n][o] (private column, no
 // atomics); the block sums its point groups in a fixed order into part[block][O][D][B] (+ part_b)
@@ -248,6 +327,162 @@ __global__ void __launch_bounds__(FL_THREADS) k_wgrad_first(const float* __restr
     } else {
       v = dbs_sh[(o / blockDim.x) * FL_THREADS + (o % blockDim.x)];
     }
+    part_b[blockIdx.x * (int64_t)O + o] = v;
+  }
+}
+
+// Weight gradient of the first layer for interior passes, accumulated in REGISTERS: thread (o, point
+// group qg) owns dW[o][a][n] for every coordinate a and every basis n < BMAX (BMAX >= B, packed pairs), and
+// each point's contribution is applied densely over n from a per-batch shared table that holds
+// v, v', v'' of every basis (zero outside the k+1 active ones):
+//   acc[a][n] += ybar_o v_n(xi_a) + ybar'_{o,a} v'_n(xi_a) + ybar''_{o,a} v''_n(xi_a)
+// -- (BMAX/(k+1))x more FMAs than the band-limited update, but no shared-memory read-modify-write
+// chain (the previous kernel serialised on it) and no branches.  Block partials part[block][O][D][B]
+// (+ part_b) are summed in a fixed order by k_reduce_parts.
+// points per batch of k_wgrad_first_r (one bulk copy of their adjoint rows): 8, or 4 when two 8-point stages
+// would exceed 72 KB (C5's 7 x 256 rows: 4 keeps two blocks per SM)
+__host__ __device__ constexpr int wf_pb(int C, int O) { return 2 * 8 * C * O * 4 <= 72 * 1024 ? 8 : 4; }
+
+template <int NF, int NS, int M, int BMAX>
+__global__ void __launch_bounds__(FL_THREADS) k_wgrad_first_r(const float* __restrict__ pts,
+                                                              const float* __restrict__ Ybar, float* __restrict__ part,
+                                                              float* __restrict__ part_b, int64_t P, int O,
+                                                              BasisCfg bc) {
+  constexpr int D = NF;
+  constexpr int C = 1 + NF + NS;
+  constexpr int NPR = BMAX / 2;                   // basis pairs
+  const int PB = wf_pb(C, O);
+  static_assert(BMAX % 4 == 0, "table rows are float4 aligned");
+  extern __shared__ __align__(16) float wsm[];
+  const int B = bc.B;
+  const int QG = (int)blockDim.x / O;
+  const int ring = max(2 * PB * C * O, QG * D * B * O);
+  float* ybs = wsm;                               // [2][PB][C][O] adjoint rows (bulk copies, 2-stage ring);
+                                                  // at the end [QG][D*B][O] accumulators
+  float* V = ybs + ring;                          // [PB][D][3][BMAX]
+  float* red = V + PB * D * 3 * BMAX;             // [FL_THREADS] fixed-order point-group reduction
+  __shared__ __align__(8) uint64_t full[2];
+  const int qg = (int)threadIdx.x / O, o = (int)threadIdx.x % O;
+  const bool active = qg < QG;
+  uint64_t acc[D][NPR];
+#pragma unroll
+  for (int a = 0; a < D; ++a)
+#pragma unroll
+    for (int j = 0; j < NPR; ++j) acc[a][j] = 0ull;   // (0.f, 0.f)
+  float dbs = 0.f;
+  const int64_t lo = (P * blockIdx.x) / gridDim.x, hi = (P * (blockIdx.x + 1)) / gridDim.x;
+  const int nbat = (int)((hi - lo + PB - 1) / PB);
+  const uint32_t row_bytes = (uint32_t)(C * O * 4);
+  auto issue = [&](int b) {                       // thread 0: batch b -> stage b & 1
+    const int64_t p0 = lo + (int64_t)b * PB;
+    const int npb = (int)((hi - p0) < PB ? (hi - p0) : PB);
+    tc::mbar_arrive_expect_tx(&full[b & 1], row_bytes * npb);
+    tc::bulk_g2s(ybs + (b & 1) * (PB * C * O), Ybar + p0 * (int64_t)(C * O), row_bytes * npb, &full[b & 1]);
+  };
+  if (threadIdx.x == 0) {
+    tc::mbar_init(&full[0], 1);
+    tc::mbar_init(&full[1], 1);
+    tc::fence_mbar_init();
+    if (nbat > 0) issue(0);
+    if (nbat > 1) issue(1);
+  }
+  for (int b = 0; b < nbat; ++b) {
+    const int64_t p0 = lo + (int64_t)b * PB;
+    const int nq = (int)((hi - p0) < PB ? (hi - p0) : PB);
+    __syncthreads();                              // previous batch's table consumed (and barrier init visible)
+    // table: task = (point q, coordinate a, 4 consecutive bases), each basis evaluated in place
+    for (int e = threadIdx.x; e < PB * D * (BMAX / 4); e += blockDim.x) {
+      const int n4 = 4 * (e % (BMAX / 4)), qa = e / (BMAX / 4);
+      const int q = qa / D, a = qa - (qa / D) * D;
+      const float x = (q < nq) ? __ldg(pts + (p0 + q) * D + a) : 0.f;
+      const int n0 = first_basis(x, bc);
+      float vd[3][4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int n = n4 + u, r = n - n0;
+        float v0 = 0.f, v1 = 0.f, v2 = 0.f, v3;
+        if (q < nq && r >= 0 && r <= bc.k && n < B) hr_eval<M, (NS > 0 ? 2 : 1)>(basis_q(x, n, bc), bc.sc, v0, v1, v2, v3);
+        if (q < nq && x != x) v0 = v1 = v2 = x;   // NaN inputs poison their row (flagged downstream)
+        vd[0][u] = v0;
+        vd[1][u] = v1;
+        vd[2][u] = v2;
+      }
+      float* row = V + qa * 3 * BMAX + n4;
+#pragma unroll
+      for (int d = 0; d < 3; ++d)
+        *reinterpret_cast<float4*>(row + d * BMAX) = make_float4(vd[d][0], vd[d][1], vd[d][2], vd[d][3]);
+    }
+    __syncthreads();
+    tc::mbar_wait(&full[b & 1], (uint32_t)((b >> 1) & 1));
+    const float* yst = ybs + (b & 1) * (PB * C * O) + o;
+    if (active) {
+      for (int q = qg; q < nq; q += QG) {
+        float y[C];
+#pragma unroll
+        for (int c = 0; c < C; ++c) y[c] = yst[(q * C + c) * O];
+        dbs += y[0];
+        const uint64_t Y0 = tc::pk2(y[0], y[0]);
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+          const uint64_t Y1 = tc::pk2(y[1 + a], y[1 + a]);
+          const float y2 = (a < NS) ? y[1 + NF + (a < NS ? a : 0)] : 0.f;
+          const uint64_t Y2 = tc::pk2(y2, y2);
+          const float4* r0 = reinterpret_cast<const float4*>(V + (q * D + a) * 3 * BMAX);
+#pragma unroll
+          for (int j4 = 0; j4 < BMAX / 4; ++j4) {
+            const float4 w0 = r0[j4], w1 = r0[BMAX / 4 + j4];
+            uint64_t a0 = acc[a][2 * j4], a1 = acc[a][2 * j4 + 1];
+            a0 = tc::fma2(Y0, tc::pk2(w0.x, w0.y), a0);
+            a1 = tc::fma2(Y0, tc::pk2(w0.z, w0.w), a1);
+            a0 = tc::fma2(Y1, tc::pk2(w1.x, w1.y), a0);
+            a1 = tc::fma2(Y1, tc::pk2(w1.z, w1.w), a1);
+            if (a < NS) {
+              const float4 w2 = r0[2 * (BMAX / 4) + j4];
+              a0 = tc::fma2(Y2, tc::pk2(w2.x, w2.y), a0);
+              a1 = tc::fma2(Y2, tc::pk2(w2.z, w2.w), a1);
+            }
+            acc[a][2 * j4] = a0;
+            acc[a][2 * j4 + 1] = a1;
+          }
+        }
+      }
+    }
+    __syncthreads();                              // stage b & 1 fully read
+    if (threadIdx.x == 0 && b + 2 < nbat) {
+      tc::fence_proxy_async_smem();               // generic reads of the stage before the async-proxy refill
+      issue(b + 2);
+    }
+  }
+  // fixed-order sum over the point groups: accumulators -> shared [QG][D*B][O] (the stage ring is free now)
+  const int64_t nW = (int64_t)O * D * B;
+  float* dst = part + (int64_t)blockIdx.x * nW;
+  float* accs = ybs;
+  __syncthreads();
+  if (active) {
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+#pragma unroll
+      for (int j = 0; j < NPR; ++j) {
+        float lo_, hi_;
+        tc::upk2(acc[a][j], lo_, hi_);
+        if (2 * j < B) accs[((qg * D + a) * B + 2 * j) * O + o] = lo_;
+        if (2 * j + 1 < B) accs[((qg * D + a) * B + 2 * j + 1) * O + o] = hi_;
+      }
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < D * B * O; e += blockDim.x) {
+    float v = 0.f;
+    for (int g = 0; g < QG; ++g) v += accs[g * D * B * O + e];
+    const int oo = e % O, an = e / O;            // accs index (a*B + n)*O + o
+    dst[(int64_t)oo * D * B + an] = v;
+  }
+  __syncthreads();
+  red[threadIdx.x] = active ? dbs : 0.f;
+  __syncthreads();
+  if (qg == 0) {
+    float v = 0.f;
+    for (int g = 0; g < QG; ++g) v += red[g * O + o];
     part_b[blockIdx.x * (int64_t)O + o] = v;
   }
 }

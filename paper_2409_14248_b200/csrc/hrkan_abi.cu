@@ -173,6 +173,7 @@ hrkan_status hrkan_create(const int32_t* widths, int32_t n_widths, int32_t G, in
   // tuning overrides for experiments (precision/speed trade-off of the TMEM drain segments)
   if (const char* e = std::getenv("HRKAN_TC_SEG")) net->tc_seg = net->tc_seg_single = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("HRKAN_TC_WSEG")) net->tc_wseg = std::max(1, std::atoi(e));
+  if (const char* e = std::getenv("HRKAN_FUSE_SPLIT")) net->fuse_split = std::atoi(e) != 0;
   if (const char* e = std::getenv("HRKAN_TC_DBG")) net->tc_dbg = std::atoi(e);
   auto cleanup = [&](hrkan_status s) {
     hrkan_free(net);

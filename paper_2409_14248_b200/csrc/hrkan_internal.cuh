@@ -140,11 +140,13 @@ struct hrkan_net {
   DevBuf tc_ws;                         // tensor-core path scratch
   DevBuf tiny_cnt;                      // k_tiny_step's finished-block counter (reset by the last block)
   DevBuf tc_yw, tc_yd;                  // pre-split bf16 hi/lo Ybar operands of the reverse kernels
+  DevBuf tc_bias_part;                  // bias-gradient partials emitted by the fused output layer (k_last_v3 SPLIT)
   std::vector<TcLayerState> tc_layers;
   int tc_seg = 96;                      // K-blocks per forward TMEM segment, double-buffered accumulators (C3/C4: one segment;
                                         // the drains run on the generator warps: C4 fwd 3.79 -> 3.11 ms, u 1.2e-5 -> 1.7e-5)
   int tc_seg_single = 160;              // ... single accumulator (the drain stalls the MMA): C5 -> 2 segments
   int tc_wseg = 256;                    // wgrad stages per TMEM drain into the fp32 master
+  bool fuse_split = true;               // output layer emits the last hidden layer's pre-split operands (HRKAN_FUSE_SPLIT)
   int tc_dbg = 0;                       // timing-experiment switches (HRKAN_TC_DBG; 0 in production)
   // CUDA-graph replay of hrkan_pinn_loss_grad (hrkan_set_graph_mode)
   bool graph_mode = false;

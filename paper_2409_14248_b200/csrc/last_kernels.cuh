@@ -580,4 +580,332 @@ __global__ void __launch_bounds__(256, 3)
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Output layer, input-parallel, loss modes only (k <= 3, I % 32 == 0): the v2 algorithm with
+//   * the batch's jets [PB points][C][I] fetched by ONE 1-D bulk copy into a 2-stage shared-memory
+//     ring (batch b+2 is in flight while b is processed: no per-thread load latency, no staging STS),
+//   * the basis values v, v', v'' of the k+1 candidates and T1..T3 = sum_n w_n v_n^(1..3) computed
+//     once in pass 1 and kept in registers for pass 2 (v2 re-evaluated the basis and reloaded W),
+//   * W and the dW accumulator in shared memory with KT-1 zero rows on each side of the B bases, so
+//     the KT candidate rows are read / updated without predicates.
+// Same arithmetic and reduction order as k_last_v2 (fixed order: deterministic).
+// ---------------------------------------------------------------------------------------------
+constexpr int LV3_PB = 4;    // points per batch
+constexpr int LV3_KT = 4;    // candidate bases per x (k + 1 <= 4)
+
+__host__ __device__ constexpr int lv3_bp(int B) { return (B + 2 * (LV3_KT - 1)) | 1; }   // odd: conflict-free rows
+
+// SPLIT: the adjoint of the input jet is not written in fp32; instead the block emits the bf16 hi/lo
+// operand stages of the preceding tensor-core layer's reverse kernels (k_split_ybar's YW / YD layouts,
+// see tc_kernels.cuh) and that layer's bias-gradient partials part_bias[block][I] -- the fp32 adjoint
+// never goes to HBM and the separate split pass disappears.  Block point ranges are multiples of 8
+// (YW's 8-point blocks: a batch of PB = 4 points is one half of one block).
+template <int NF, int NS, int M, int MODE, bool SPLIT>
+__global__ void __launch_bounds__(256, 2)
+    k_last_v3(const float* __restrict__ X, const float* __restrict__ W, const float* __restrict__ bias, int64_t P,
+              int I, BasisCfg bc, const float* __restrict__ pts, const float* __restrict__ forcing,
+              const float* __restrict__ gtar, float alpha, float adv, float visc, float inv_n, float* __restrict__ Xbar,
+              float* __restrict__ part, uint16_t* __restrict__ YW, uint16_t* __restrict__ YD,
+              float* __restrict__ part_bias) {
+  constexpr int C = 1 + NF + NS;
+  constexpr int D = (MODE == LAST_POISSON) ? NF : 2;
+  constexpr int PB = LV3_PB, KT = LV3_KT, KO = KT - 1;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nw = blockDim.x >> 5;                 // = I / 32
+  const int i = threadIdx.x;
+  const int B = bc.B, BP = lv3_bp(B);
+  extern __shared__ __align__(16) float sm3[];
+  const int STG = PB * C * (I + 4);               // stage floats: jets [PB][C][I], or (SPLIT) the adjoint [PB*C][I+4]
+  float* jst = sm3;                               // [2][STG] jet stages (bulk copies)
+  float* Ws = jst + 2 * STG;                      // [I][BP]   W[0][i][n] at column KO + n
+  float* acc = Ws + I * BP;                       // [BP][I]   dW rows KO + n
+  float* wpart = acc + BP * I;                    // [PB][nw][C]
+  float* ys = wpart + PB * nw * C;                // [PB][C]
+  __shared__ __align__(8) uint64_t full[2];
+  __shared__ float red[3][PB];
+  for (int t = threadIdx.x; t < I * BP; t += blockDim.x) {
+    const int ii = t / BP, n = t - ii * BP - KO;
+    Ws[t] = (n >= 0 && n < B) ? __ldg(W + ii * B + n) : 0.f;
+    acc[t] = 0.f;
+  }
+  const int64_t nb8 = (P + 7) / 8;                // 8-point blocks (block ranges are whole blocks)
+  const int64_t lo = 8 * ((nb8 * blockIdx.x) / gridDim.x);
+  const int64_t hi = min(P, 8 * ((nb8 * (blockIdx.x + 1)) / gridDim.x));
+  const int nbat = (int)((hi - lo + PB - 1) / PB);
+  const uint32_t row_bytes = (uint32_t)(C * I * 4);
+  auto issue = [&](int b) {                       // thread 0: batch b -> stage b & 1
+    const int64_t p0 = lo + (int64_t)b * PB;
+    const int npb = (int)((hi - p0) < PB ? (hi - p0) : PB);
+    tc::mbar_arrive_expect_tx(&full[b & 1], row_bytes * npb);
+    tc::bulk_g2s(jst + (b & 1) * STG, X + p0 * (int64_t)(C * I), row_bytes * npb, &full[b & 1]);
+  };
+  if (threadIdx.x == 0) {
+    tc::mbar_init(&full[0], 1);
+    tc::mbar_init(&full[1], 1);
+    tc::fence_mbar_init();
+    if (nbat > 0) issue(0);
+    if (nbat > 1) issue(1);
+  }
+  __syncthreads();
+  const float b0 = __ldg(bias);
+  const float sc = bc.sc;
+  float db = 0.f, sq = 0.f, bad = 0.f;            // thread q < PB accumulates its batch slot
+  float dbi = 0.f;                                // SPLIT: bias gradient of the preceding layer, output i
+  for (int b = 0; b < nbat; ++b) {
+    const int64_t p0 = lo + (int64_t)b * PB;
+    const int npb = (int)((hi - p0) < PB ? (hi - p0) : PB);
+    const float* J = jst + (b & 1) * STG + i;
+    tc::mbar_wait(&full[b & 1], (uint32_t)((b >> 1) & 1));
+    // ---------------- pass 1: output-jet partials; cache the candidate basis values and T1..T3
+    constexpr int NVT = PB * C;
+    constexpr int NV = NVT <= 4 ? 4 : NVT <= 8 ? 8 : NVT <= 16 ? 16 : 32;
+    static_assert(NVT <= 32, "batch x channels must fit one warp");
+    float V[NV];
+#pragma unroll
+    for (int k = 0; k < NV; ++k) V[k] = 0.f;
+    float cv[PB][3][KT], cT[PB][3];
+    int cn[PB];
+#pragma unroll
+    for (int q = 0; q < PB; ++q) {
+      cn[q] = 0;
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        cT[q][d] = 0.f;
+#pragma unroll
+        for (int r = 0; r < KT; ++r) cv[q][d][r] = 0.f;
+      }
+      if (q >= npb) continue;
+      const float* jq = J + q * C * I;
+      const float x = jq[0];
+      const int n0 = first_basis(x, bc);
+      uint64_t P0 = 0ull, P1 = 0ull, P2 = 0ull, P3 = 0ull;
+#pragma unroll
+      for (int r = 0; r < KT; r += 2) {
+        const int na = n0 + r, nb = na + 1;
+        const bool oka = r <= bc.k && na >= 0 && na < B, okb = r + 1 <= bc.k && nb >= 0 && nb < B;
+        uint64_t v0, v1, v2, v3;
+        hr_eval_pair<M>(x, na, nb, oka, okb, bc, v0, v1, v2, v3);
+        tc::upk2(v0, cv[q][0][r], cv[q][0][r + 1]);
+        tc::upk2(v1, cv[q][1][r], cv[q][1][r + 1]);
+        tc::upk2(v2, cv[q][2][r], cv[q][2][r + 1]);
+        // W rows of the candidates (zero rows outside [0, B)); n0 clamped below keeps them in range
+        const int nc = min(max(n0, -KO), B - 1);
+        const float* wr = Ws + i * BP + KO + nc + r;
+        const uint64_t w = tc::pk2((n0 == nc) ? wr[0] : 0.f, (n0 == nc) ? wr[1] : 0.f);
+        P0 = tc::fma2(w, v0, P0);
+        P1 = tc::fma2(w, v1, P1);
+        P2 = tc::fma2(w, v2, P2);
+        P3 = tc::fma2(w, v3, P3);
+      }
+      cn[q] = min(max(n0, -KO), B - 1);           // all candidates zero when n0 was clamped
+      float lo_, hi_, T0;
+      tc::upk2(P0, lo_, hi_); T0 = lo_ + hi_;
+      tc::upk2(P1, lo_, hi_); cT[q][0] = lo_ + hi_;
+      tc::upk2(P2, lo_, hi_); cT[q][1] = lo_ + hi_;
+      tc::upk2(P3, lo_, hi_); cT[q][2] = lo_ + hi_;
+      float s[C];
+      s[0] = (x != x) ? x : T0;                   // propagate NaN inputs into the residual / flag
+#pragma unroll
+      for (int a = 0; a < NF; ++a) s[1 + a] = cT[q][0] * jq[(1 + a) * I];
+#pragma unroll
+      for (int a = 0; a < NS; ++a) {
+        const float d1 = jq[(1 + a) * I], d2 = jq[(1 + NF + a) * I];
+        s[1 + NF + a] = fmaf(cT[q][1] * d1, d1, cT[q][0] * d2);
+      }
+#pragma unroll
+      for (int c = 0; c < C; ++c) V[q * C + c] = s[c];
+    }
+    {
+      const float tot = warp_sum_transpose<NV>(V, lane);   // lane l: warp total of value l % NV
+      if (lane < NVT && lane / C < npb) wpart[((lane / C) * nw + warp) * C + lane % C] = tot;
+    }
+    __syncthreads();
+    // ---------------- totals, residual, loss, seeds (thread q per point)
+    if (threadIdx.x < npb) {
+      const int q = threadIdx.x;
+      const int64_t p = p0 + q;
+      float s[C];
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        float v = 0.f;
+        for (int w = 0; w < nw; ++w) v += wpart[(q * nw + w) * C + c];
+        s[c] = v;
+      }
+      s[0] += b0;
+      float y[C];
+#pragma unroll
+      for (int c = 0; c < C; ++c) y[c] = 0.f;
+      float r;
+      if (MODE == LAST_BOUNDARY) {
+        r = s[0] - __ldg(gtar + p);
+        y[0] = 2.f * r * inv_n;
+      } else if (MODE == LAST_BURGERS) {
+        r = s[2] + adv * s[0] * s[1] - visc * s[1 + NF];
+        const float g = 2.f * alpha * r * inv_n;
+        y[0] = g * adv * s[1];
+        y[1] = g * adv * s[0];
+        y[2] = g;
+        y[1 + NF] = -g * visc;
+      } else {
+        float f;
+        if (forcing) {
+          f = __ldg(forcing + p);
+        } else {
+          float prod = 1.f;
+#pragma unroll
+          for (int a = 0; a < D; ++a) prod *= sinpif(__ldg(pts + p * D + a));
+          f = -(float)D * 9.8696044010893586f * prod;   // -D pi^2 prod_a sin(pi xi_a)
+        }
+        float lap = 0.f;
+#pragma unroll
+        for (int a = 0; a < NS; ++a) lap += s[1 + NF + a];
+        r = lap - f;
+        const float g = 2.f * alpha * r * inv_n;
+#pragma unroll
+        for (int a = 0; a < NS; ++a) y[1 + NF + a] = g;
+      }
+      sq = fmaf(r, r, sq);
+      bad += isfinite(r) ? 0.f : 1.f;
+      db += y[0];
+#pragma unroll
+      for (int c = 0; c < C; ++c) ys[q * C + c] = y[c];
+    }
+    __syncthreads();
+    // ---------------- pass 2: dW and the adjoint of the input jet, from the cached values
+    float ov[PB][C];                              // (SPLIT) this thread's adjoint values of the batch
+#pragma unroll
+    for (int q = 0; q < PB; ++q)
+#pragma unroll
+      for (int c = 0; c < C; ++c) ov[q][c] = 0.f;
+#pragma unroll
+    for (int q = 0; q < PB; ++q) {
+      if (q >= npb) break;
+      const int64_t p = p0 + q;
+      const float* jq = J + q * C * I;
+      float y[C];
+#pragma unroll
+      for (int c = 0; c < C; ++c) y[c] = ys[q * C + c];
+      float dx[NF > 0 ? NF : 1], ddx[NS > 0 ? NS : 1];
+#pragma unroll
+      for (int a = 0; a < NF; ++a) dx[a] = jq[(1 + a) * I];
+#pragma unroll
+      for (int a = 0; a < NS; ++a) ddx[a] = jq[(1 + NF + a) * I];
+      float g1 = 0.f, g2 = 0.f;
+#pragma unroll
+      for (int a = 0; a < NF; ++a) g1 = fmaf(y[1 + a], dx[a], g1);
+#pragma unroll
+      for (int a = 0; a < NS; ++a) {
+        g1 = fmaf(y[1 + NF + a], ddx[a], g1);
+        g2 = fmaf(y[1 + NF + a] * dx[a], dx[a], g2);
+      }
+      float* ar = acc + (KO + cn[q]) * I + i;
+#pragma unroll
+      for (int r = 0; r < KT; ++r) ar[r * I] += fmaf(y[0], cv[q][0][r], fmaf(g1, cv[q][1][r], g2 * cv[q][2][r]));
+      const float T1 = cT[q][0], T2 = cT[q][1], T3 = cT[q][2];
+      ov[q][0] = fmaf(y[0], T1, fmaf(g1, T2, g2 * T3));
+#pragma unroll
+      for (int a = 0; a < NF; ++a) {
+        float v = y[1 + a] * T1;
+        if (a < NS) v = fmaf(2.f * y[1 + NF + a] * dx[a], T2, v);
+        ov[q][1 + a] = v;
+      }
+#pragma unroll
+      for (int a = 0; a < NS; ++a) ov[q][1 + NF + a] = y[1 + NF + a] * T1;
+      if constexpr (!SPLIT) {
+        float* out = Xbar + p * (int64_t)(C * I) + i;
+#pragma unroll
+        for (int c = 0; c < C; ++c) out[c * I] = ov[q][c];
+      }
+    }
+    __syncthreads();                              // stage b & 1 fully read
+    if constexpr (SPLIT) {
+      // the adjoint of the batch -> stage (rows q*C + c, stride I + 4), then the bf16 hi/lo operand stages
+      constexpr int NP = tc_np(C), N = NP * C;
+      float* xs = jst + (b & 1) * STG;
+#pragma unroll
+      for (int q = 0; q < PB; ++q) {
+        dbi += ov[q][0];
+#pragma unroll
+        for (int c = 0; c < C; ++c) xs[(q * C + c) * (I + 4) + i] = ov[q][c];
+      }
+      __syncthreads();
+      // YW (wgrad B operand): chunk z = block*C + c of 8 points; this batch is half (p0 / 4) & 1
+      const int64_t b8 = p0 >> 3;
+      const int half = (int)((p0 >> 2) & 1);
+      for (int t = threadIdx.x; t < C * I; t += blockDim.x) {
+        const int c = t / I, o = t - c * I;
+        const float4 v = make_float4(xs[c * (I + 4) + o], xs[(C + c) * (I + 4) + o], xs[(2 * C + c) * (I + 4) + o],
+                                     xs[(3 * C + c) * (I + 4) + o]);
+        uint2 h, l;
+        tc::split4_bf16(v, h, l);
+        const int64_t z = b8 * C + c;
+        uint16_t* dst = YW + (z >> 1) * (int64_t)(4 * I * 8) + ((z & 1) * I + o) * 8 + half * 4;
+        *reinterpret_cast<uint2*>(dst) = h;
+        *reinterpret_cast<uint2*>(dst + 2 * I * 8) = l;
+      }
+      // YD (dgrad B operand): row p*C + c of the point tile, 8 consecutive outputs per 16 B
+      const int64_t tile = p0 / NP;
+      const int row0 = (int)(p0 - tile * NP) * C;
+      const int nkb = I / 16;
+      for (int t = threadIdx.x; t < PB * C * (I / 8); t += blockDim.x) {
+        const int rw = t % (PB * C), og = t / (PB * C);
+        const float4* sp = reinterpret_cast<const float4*>(xs + rw * (I + 4) + og * 8);
+        const float4 a0 = sp[0], a1 = sp[1];
+        float v[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+        uint4 h, l;
+        tc::split8_bf16(v, h, l);
+        uint16_t* dst = YD + (tile * nkb + og / 2) * (int64_t)(4 * N * 8) + ((og & 1) * N + row0 + rw) * 8;
+        *reinterpret_cast<uint4*>(dst) = h;
+        *reinterpret_cast<uint4*>(dst + 2 * N * 8) = l;
+      }
+      __syncthreads();                            // stage read by the emitters
+    }
+    if (threadIdx.x == 0 && b + 2 < nbat) {
+      tc::fence_proxy_async_smem();               // generic reads of the stage before the async-proxy refill
+      issue(b + 2);
+    }
+  }
+  if constexpr (SPLIT) {
+    part_bias[(int64_t)blockIdx.x * I + i] = dbi;
+    if (hi == P && lo < P) {                      // the block holding the last point: YW tails
+      const int rem = (int)(P & 7);
+      if (rem >= 1 && rem <= 4) {                 // last 8-point block: its second half has no batch
+        for (int t = threadIdx.x; t < C * I; t += blockDim.x) {
+          const int c = t / I, o = t - c * I;
+          const int64_t z = (nb8 - 1) * C + c;
+          uint16_t* dst = YW + (z >> 1) * (int64_t)(4 * I * 8) + ((z & 1) * I + o) * 8 + 4;
+          *reinterpret_cast<uint2*>(dst) = make_uint2(0u, 0u);
+          *reinterpret_cast<uint2*>(dst + 2 * I * 8) = make_uint2(0u, 0u);
+        }
+      }
+      if ((nb8 * C) & 1) {                        // odd chunk total: zero the final half-stage
+        const int64_t z = nb8 * C;
+        for (int o = threadIdx.x; o < I; o += blockDim.x) {
+          uint16_t* dst = YW + (z >> 1) * (int64_t)(4 * I * 8) + (I + o) * 8;
+          *reinterpret_cast<uint4*>(dst) = make_uint4(0u, 0u, 0u, 0u);
+          *reinterpret_cast<uint4*>(dst + 2 * I * 8) = make_uint4(0u, 0u, 0u, 0u);
+        }
+      }
+    }
+  }
+  // ---------------- fixed-order block reduction -> part[block][IB + 4]
+  if (threadIdx.x < PB) {
+    red[0][threadIdx.x] = db;
+    red[1][threadIdx.x] = sq;
+    red[2][threadIdx.x] = bad;
+  }
+  __syncthreads();
+  float* dst = part + (size_t)blockIdx.x * (I * B + 4);
+  for (int t = threadIdx.x; t < I * B; t += blockDim.x) {
+    const int ii = t / B, n = t - ii * B;
+    dst[t] = acc[(KO + n) * I + ii];              // flat W layout [i][n]
+  }
+  if (threadIdx.x < 3) {
+    float v = 0.f;
+#pragma unroll
+    for (int q = 0; q < PB; ++q) v += red[threadIdx.x][q];
+    dst[I * B + threadIdx.x] = v;
+  }
+}
+
 }  // namespace

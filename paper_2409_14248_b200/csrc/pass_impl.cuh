@@ -4,21 +4,63 @@
 #pragma once
 #include "hrkan_internal.cuh"
 #include "simt_kernels.cuh"
+#include "tc_kernels.cuh"
 #include "last_kernels.cuh"
 #include "first_kernels.cuh"
 #include "tiny_kernels.cuh"
-#include "tc_kernels.cuh"
 #include "jet_kernels.cuh"
 
 namespace {
 
+// want_split: the preceding hidden layer runs both reverse kernels on the tensor cores, so the output layer may
+// emit their pre-split bf16 operands and bias partials directly (k_last_v3<..., SPLIT>); *split_nb is then set
+// to the number of bias-partial rows in net->tc_bias_part (0 when the fp32 adjoint was written instead).
 template <int NF, int NS, int M, int MODE, bool FIRST>
 hrkan_status launch_last(hrkan_net* net, const float* in, int64_t n, const PassArgs& a, int64_t c0, float* xbar,
-                         cudaStream_t st) {
+                         cudaStream_t st, bool want_split = false, int* split_nb = nullptr) {
+  if (split_nb) *split_nb = 0;
   const int l = net->L - 1;
   const int I = net->widths[l];
   const int IB = I * net->B;
   constexpr int C = 1 + NF + NS;
+  if constexpr (!FIRST && MODE != LAST_JET && M >= 4) {
+    if (I % 32 == 0 && I <= 256 && net->bc.k + 1 <= LV3_KT) {
+      // input-parallel, bulk-copied jet batches, cached basis values (k_last_v3)
+      constexpr bool CAN_SPLIT = tc_np(C) > 0;
+      const bool split = CAN_SPLIT && want_split && split_nb;
+      auto kv = split ? k_last_v3<NF, NS, M, MODE, CAN_SPLIT> : k_last_v3<NF, NS, M, MODE, false>;
+      const int nw = I / 32, BP = lv3_bp(net->B);
+      const size_t smem = sizeof(float) * ((size_t)2 * LV3_PB * C * (I + 4) + 2 * (size_t)I * BP + (size_t)LV3_PB * nw * C + LV3_PB * C);
+      HR_CUDA(smem_optin(kv, smem));
+      int per_sm = 0;
+      HR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kv, I, smem));
+      per_sm = std::max(1, per_sm);
+      const int nb = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)per_sm * net->num_sms, (n + LV3_PB - 1) / LV3_PB));
+      HR_CUDA(net->last_part.ensure(sizeof(float) * (size_t)nb * (IB + 4)));
+      const hrkan_pde* pde = a.pde;
+      const float* pts = a.pts + c0 * net->D;
+      const float* f = a.forcing ? a.forcing + c0 : nullptr;
+      const float* g = a.g ? a.g + c0 : nullptr;
+      uint16_t *yw = nullptr, *yd = nullptr;
+      float* pbias = nullptr;
+      if (split) {
+        if constexpr (CAN_SPLIT) HR_TRY(tc_split_buffers<C>(net, I, n));
+        HR_CUDA(net->tc_bias_part.ensure(sizeof(float) * (size_t)nb * I));
+        yw = (uint16_t*)net->tc_yw.p;
+        yd = (uint16_t*)net->tc_yd.p;
+        pbias = net->tc_bias_part.f();
+        *split_nb = nb;
+      }
+      HR_LAUNCH(HRKAN_K_FWD_LAST, split ? "k_last_v3 (split)" : "k_last_v3",
+                kv<<<nb, I, smem, st>>>(in, net->params + net->w_off[l], net->params + net->b_off[l], n, I, net->bc, pts, f,
+                                        g, pde->alpha, pde->adv, pde->visc, a.inv_n, xbar, net->last_part.f(), yw, yd, pbias));
+      const float scale = (MODE == LAST_BOUNDARY) ? a.inv_n : pde->alpha * a.inv_n;
+      HR_LAUNCH(HRKAN_K_REDUCE, "k_reduce_last",
+                k_reduce_last<<<(IB + 3 + RL_COLS - 1) / RL_COLS, RL_COLS * RL_CHAINS, 0, st>>>(net->last_part.f(), nb, IB, a.grad + net->w_off[l],
+                                                                     a.grad + net->b_off[l], scale, a.out_loss, a.out_flag));
+      return HRKAN_OK;
+    }
+  }
   if (!FIRST && I % 32 == 0 && I <= 256) {
     // input-parallel variant: I/32 warps per block, block-shared dW accumulator
     auto kv = k_last_v2<NF, NS, M, MODE>;
@@ -87,6 +129,64 @@ hrkan_status launch_last(hrkan_net* net, const float* in, int64_t n, const PassA
   return HRKAN_OK;
 }
 
+// First-layer forward with W staged in shared memory (k_fwd_first_s) when it fits; *done = false otherwise.
+template <int NF, int NS, int M>
+hrkan_status launch_fwd_first_s(hrkan_net* net, const float* X0, float* Y, int64_t n, int O, cudaStream_t st, bool* done) {
+  *done = false;
+  const int B = net->B;
+  if (O > FL_THREADS || net->bc.k + 1 > KMAX) return HRKAN_OK;
+  auto go = [&](auto KTc) -> hrkan_status {
+    constexpr int KT = decltype(KTc)::value;
+    const size_t smem = sizeof(FlTab<KT>) * FL_BATCH * NF + sizeof(float) * (size_t)NF * (B + 2 * KT) * O;
+    if (smem > 200 * 1024) return HRKAN_OK;
+    auto kfn = k_fwd_first_s<NF, NS, M, KT>;
+    HR_CUDA(smem_optin(kfn, smem));
+    int per_sm = 0;
+    HR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, FL_THREADS, smem));
+    per_sm = std::max(1, per_sm);
+    const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + FL_BATCH - 1) / FL_BATCH, (int64_t)per_sm * net->num_sms));
+    HR_LAUNCH(HRKAN_K_FWD_FIRST, "k_fwd_first_s",
+              kfn<<<g, FL_THREADS, smem, st>>>(X0, net->wt[0], net->params + net->b_off[0], Y, n, O, net->bc));
+    *done = true;
+    return HRKAN_OK;
+  };
+  if (net->bc.k + 1 <= 4) return go(std::integral_constant<int, 4>{});
+  return go(std::integral_constant<int, 8>{});
+}
+
+// First-layer weight gradient with register accumulators (k_wgrad_first_r) for B <= 20; *done = false otherwise.
+template <int NF, int NS, int M>
+hrkan_status launch_wgrad_first_r(hrkan_net* net, const float* X0, const float* Ybar, float* dW, float* db, int64_t n,
+                                  int O, cudaStream_t st, bool* done) {
+  *done = false;
+  const int B = net->B;
+  if (O > FL_THREADS || B > 20 || ((1 + NF + NS) * O * 4) % 16 != 0) return HRKAN_OK;
+  auto go = [&](auto BMc) -> hrkan_status {
+    constexpr int BMAX = decltype(BMc)::value;
+    auto kfn = k_wgrad_first_r<NF, NS, M, BMAX>;
+    const int pb = wf_pb(1 + NF + NS, O);
+    const size_t ring = std::max<size_t>((size_t)2 * pb * (1 + NF + NS) * O, (size_t)(FL_THREADS / O) * NF * B * O);
+    const size_t smem = sizeof(float) * (ring + (size_t)pb * NF * 3 * BMAX + FL_THREADS);
+    HR_CUDA(smem_optin(kfn, smem));
+    int per_sm = 0;
+    HR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, FL_THREADS, smem));
+    per_sm = std::max(1, per_sm);
+    const int nzf = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)per_sm * net->num_sms, n / 64));
+    const int64_t nWf = (int64_t)O * NF * B;
+    HR_CUDA(net->first_part.ensure(sizeof(float) * (size_t)nzf * (nWf + O)));
+    float* fpart = net->first_part.f();
+    float* fpart_b = fpart + (size_t)nzf * nWf;
+    HR_LAUNCH(HRKAN_K_WGRAD_FIRST, "k_wgrad_first_r", kfn<<<nzf, FL_THREADS, smem, st>>>(X0, Ybar, fpart, fpart_b, n, O, net->bc));
+    HR_LAUNCH(HRKAN_K_REDUCE, "k_reduce_parts",
+              k_reduce_parts<<<(unsigned)((nWf + O + 255) / 256), 256, 0, st>>>(fpart, fpart_b, nzf, nWf, O, dW, db));
+    *done = true;
+    return HRKAN_OK;
+  };
+  if (B <= 12) return go(std::integral_constant<int, 12>{});
+  if (B <= 16) return go(std::integral_constant<int, 16>{});
+  return go(std::integral_constant<int, 20>{});
+}
+
 // Forward + (optional) loss/seeds + reverse over one point set, chunk by chunk.
 template <int NF, int NS, int M>
 hrkan_status run_pass(hrkan_net* net, const PassArgs& a, cudaStream_t st) {
@@ -119,8 +219,12 @@ hrkan_status run_pass(hrkan_net* net, const PassArgs& a, cudaStream_t st) {
         const int cls = (l == 0) ? HRKAN_K_FWD_FIRST : HRKAN_K_FWD_HIDDEN;
         if (l == 0) {
           const int bd = FL_THREADS;
-          const unsigned gf = (unsigned)std::min<int64_t>((n + FL_BATCH - 1) / FL_BATCH, 16 * net->num_sms);
-          HR_LAUNCH(cls, "k_fwd_first", k_fwd_first<NF, NS, M><<<gf, bd, 0, st>>>(in, net->wt[l], net->params + net->b_off[l], jet[l + 1], n, I, O, bc));
+          bool fast = false;
+          if constexpr (NF > 0) HR_TRY(launch_fwd_first_s<NF, NS, M>(net, in, jet[l + 1], n, O, st, &fast));
+          if (!fast) {
+            const unsigned gf = (unsigned)std::min<int64_t>((n + FL_BATCH - 1) / FL_BATCH, 16 * net->num_sms);
+            HR_LAUNCH(cls, "k_fwd_first", k_fwd_first<NF, NS, M><<<gf, bd, 0, st>>>(in, net->wt[l], net->params + net->b_off[l], jet[l + 1], n, I, O, bc));
+          }
         } else
           HR_LAUNCH(cls, "k_fwd_simt", k_fwd_simt<NF, NS, M, false><<<grid, 256, 0, st>>>(in, net->wt[l], net->params + net->b_off[l], jet[l + 1], n, I, O, bc));
       }
@@ -136,10 +240,14 @@ hrkan_status run_pass(hrkan_net* net, const PassArgs& a, cudaStream_t st) {
       }
       continue;
     }
+    // the output layer emits the last hidden layer's pre-split reverse operands when that layer runs both
+    // reverse kernels on the tensor cores (HRKAN_FUSE_SPLIT=0 in the environment at create time disables it)
+    const bool want_split = L >= 3 && net->fuse_split && tc_reverse_ok(net, L - 2, n);
+    int split_nb = 0;
     auto last = [&](auto MODEc) -> hrkan_status {
       constexpr int MODE = decltype(MODEc)::value;
       if (L == 1) return launch_last<NF, NS, M, MODE, true>(net, in_last, n, a, c0, nullptr, st);
-      return launch_last<NF, NS, M, MODE, false>(net, in_last, n, a, c0, ybar, st);
+      return launch_last<NF, NS, M, MODE, false>(net, in_last, n, a, c0, ybar, st, want_split, &split_nb);
     };
     if (a.kind == PASS_INTERIOR) {
       if (a.pde->kind == HRKAN_BURGERS) {
@@ -160,8 +268,10 @@ hrkan_status run_pass(hrkan_net* net, const PassArgs& a, cudaStream_t st) {
       float* dW = a.grad + net->w_off[l];
       float* db = a.grad + net->b_off[l];
       bool done = false;
-      if (l > 0) HR_TRY(tc_split_ybar<NF, NS, M>(net, l, ybar, n, st));   // bf16 hi/lo operands of both kernels
-      if (l > 0) HR_TRY(tc_wgrad_layer<NF, NS, M>(net, l, in, ybar, dW, db, n, st, &done));
+      const bool fused = (l == L - 2) && split_nb > 0;   // operands + bias partials from the output layer
+      if (l > 0 && !fused) HR_TRY(tc_split_ybar<NF, NS, M>(net, l, ybar, n, st));   // bf16 hi/lo operands of both kernels
+      if (l > 0) HR_TRY(tc_wgrad_layer<NF, NS, M>(net, l, in, ybar, dW, db, n, st, &done,
+                                                 fused ? net->tc_bias_part.f() : nullptr, split_nb));
       if (!done) {
         const dim3 blk(WG_J, WG_I);
         const int gx = (O + WG_J - 1) / WG_J, gy = (I + WG_I - 1) / WG_I;
@@ -172,6 +282,9 @@ hrkan_status run_pass(hrkan_net* net, const PassArgs& a, cudaStream_t st) {
         const size_t smem = sizeof(float) * WG_I * net->B * WG_J;
         const int cls = (l == 0) ? HRKAN_K_WGRAD_FIRST : HRKAN_K_WGRAD_HIDDEN;
         if (l == 0) {
+          bool fast = false;
+          if constexpr (NF > 0) HR_TRY(launch_wgrad_first_r<NF, NS, M>(net, in, ybar, dW, db, n, O, st, &fast));
+          if (fast) continue;
           // first layer: batched shared basis tables, one thread per output neuron
           auto kfn = k_wgrad_first<NF, NS, M>;
           const int QG = O <= FL_THREADS ? FL_THREADS / O : 1;

@@ -631,6 +631,25 @@ hrkan_status tc_forward_layer(hrkan_net* net, int l, const float* X, float* Y, i
   }
 }
 
+// Sizes the pre-split operand buffers (net->tc_yw, net->tc_yd) of a C-channel layer with O outputs, n points.
+template <int C>
+hrkan_status tc_split_buffers(hrkan_net* net, int O, int64_t n) {
+  const int64_t nb8 = (n + 7) / 8;
+  const int64_t ntile = (n + tc_np(C) - 1) / tc_np(C);
+  const size_t yw = (size_t)((nb8 * C + 1) / 2) * 2 * 2 * O * 8;        // densely packed K chunks
+  const size_t yd = (size_t)ntile * (O / TC_KB) * 2 * 2 * tc_np(C) * C * 8;
+  HR_CUDA(net->tc_yw.ensure(yw * sizeof(uint16_t)));
+  HR_CUDA(net->tc_yd.ensure(yd * sizeof(uint16_t)));
+  return HRKAN_OK;
+}
+
+// Both reverse kernels of hidden layer l run on the tensor cores for n points (so its Ybar is consumed only
+// as the pre-split operands + bias partials, and an upstream kernel may emit those instead of fp32 Ybar).
+bool tc_reverse_ok(const hrkan_net* net, int l, int64_t n) {
+  return tc_layer_ok(net, l) && n >= 8 && l < (int)net->tc_layers.size() && net->tc_layers[l].w_dgr &&
+         dgr_tile_ok(net->B, net->D);
+}
+
 // Pre-split Ybar of tensor-core layer l for both reverse kernels (net->tc_yw, net->tc_yd).
 template <int NF, int NS, int M>
 hrkan_status tc_split_ybar(hrkan_net* net, int l, const float* Ybar, int64_t n, cudaStream_t st) {
@@ -641,11 +660,7 @@ hrkan_status tc_split_ybar(hrkan_net* net, int l, const float* Ybar, int64_t n, 
     if (!tc_layer_ok(net, l) || n <= 0) return HRKAN_OK;
     const int O = net->widths[l + 1];
     const int64_t nb8 = (n + 7) / 8;
-    const int64_t ntile = (n + tc_np(C) - 1) / tc_np(C);
-    const size_t yw = (size_t)((nb8 * C + 1) / 2) * 2 * 2 * O * 8;        // densely packed K chunks
-    const size_t yd = (size_t)ntile * (O / TC_KB) * 2 * 2 * tc_np(C) * C * 8;
-    HR_CUDA(net->tc_yw.ensure(yw * sizeof(uint16_t)));
-    HR_CUDA(net->tc_yd.ensure(yd * sizeof(uint16_t)));
+    HR_TRY(tc_split_buffers<C>(net, O, n));
     auto launch = [&](auto OC) -> hrkan_status {
       constexpr int OO = decltype(OC)::value;
       auto kfn = k_split_ybar<C, OO>;
@@ -663,7 +678,7 @@ hrkan_status tc_split_ybar(hrkan_net* net, int l, const float* Ybar, int64_t n, 
 
 template <int NF, int NS, int M, int OO>
 hrkan_status launch_wgrad_tc(hrkan_net* net, int l, const float* X, const float* Ybar, float* dW, float* db,
-                             int64_t n, cudaStream_t st) {
+                             int64_t n, cudaStream_t st, const float* bias_part, int bias_nz) {
   using Cfg = WgrCfg<NF, NS, M, OO>;
   constexpr int C = Cfg::C, O = Cfg::O;
   auto kfn = k_wgrad_tc<NF, NS, M, OO>;
@@ -703,6 +718,10 @@ hrkan_status launch_wgrad_tc(hrkan_net* net, int l, const float* X, const float*
   }
   HR_LAUNCH(HRKAN_K_REDUCE, "k_reduce_slabs",
             k_reduce_slabs<<<(unsigned)((O * K + 255) / 256), 256, 0, st>>>(part, nslab, (int64_t)O * K, dW));
+  if (bias_part) {                                   // emitted by the fused output layer
+    HR_LAUNCH(HRKAN_K_REDUCE, "k_reduce_bias", k_reduce_bias<<<(O + 31) / 32, 256, 0, st>>>(bias_part, bias_nz, O, db));
+    return HRKAN_OK;
+  }
   const int nz = (int)std::min<int64_t>(1024, std::max<int64_t>(1, n / 256));
   HR_LAUNCH(HRKAN_K_REDUCE, "k_bias_part",
             k_bias_part<<<dim3((O + 127) / 128, nz), 128, 0, st>>>(Ybar, C, O, n, part_b));
@@ -712,13 +731,13 @@ hrkan_status launch_wgrad_tc(hrkan_net* net, int l, const float* X, const float*
 
 template <int NF, int NS, int M>
 hrkan_status tc_wgrad_layer(hrkan_net* net, int l, const float* X, const float* Ybar, float* dW, float* db, int64_t n,
-                            cudaStream_t st, bool* done) {
+                            cudaStream_t st, bool* done, const float* bias_part = nullptr, int bias_nz = 0) {
   *done = false;
   if (!tc_layer_ok(net, l) || n < 8) return HRKAN_OK;
   const int O = net->widths[l + 1];
-  if (O == 64) HR_TRY(launch_wgrad_tc<NF, NS, M, 64>(net, l, X, Ybar, dW, db, n, st));
-  else if (O == 128) HR_TRY(launch_wgrad_tc<NF, NS, M, 128>(net, l, X, Ybar, dW, db, n, st));
-  else HR_TRY(launch_wgrad_tc<NF, NS, M, 256>(net, l, X, Ybar, dW, db, n, st));
+  if (O == 64) HR_TRY(launch_wgrad_tc<NF, NS, M, 64>(net, l, X, Ybar, dW, db, n, st, bias_part, bias_nz));
+  else if (O == 128) HR_TRY(launch_wgrad_tc<NF, NS, M, 128>(net, l, X, Ybar, dW, db, n, st, bias_part, bias_nz));
+  else HR_TRY(launch_wgrad_tc<NF, NS, M, 256>(net, l, X, Ybar, dW, db, n, st, bias_part, bias_nz));
   *done = true;
   return HRKAN_OK;
 }

@@ -122,6 +122,36 @@ def test_empty_sets_tensor_core_path(torch_mod, key):
     _check_loss_grad(out, w, *_loss_grad_oracle(w, params, e3))
 
 
+# ------------------------------------------------------------------ output layer emitting the split operands
+@pytest.mark.parametrize("key", ["C3", "C4", "C5"])
+@pytest.mark.parametrize("n_int", [35, 1029, 4001])
+def test_fused_split_operands_ragged(torch_mod, key, n_int, monkeypatch):
+    """k_last_v3<SPLIT> writes the last hidden layer's pre-split reverse operands (YW / YD) and its bias
+    partials itself instead of the fp32 adjoint.  Ragged sizes: n % 8 in 1..4 with no batch for the last
+    8-point block's second half (35, 4001: zero-filled by the kernel), an odd number of 8-point-block x
+    channel chunks for C = 5, 7 (zero final half-stage), and 1500-point chunks (ragged per-chunk tails).
+    Against the unfused path (HRKAN_FUSE_SPLIT=0: fp32 adjoint + k_split_ybar + k_bias_part) and the oracle."""
+    torch = torch_mod
+    w = HI.WORKLOADS[key]
+    ps0 = HI.make_points(w)
+    step = max(1, len(ps0.interior) // n_int)
+    c = np.ascontiguousarray
+    sb = max(1, len(ps0.boundary) // 21)
+    ps = HI.PointSet(c(ps0.interior[::step][:n_int]), c(ps0.boundary[::sb][:21]), c(ps0.g_boundary[::sb][:21]),
+                     None if ps0.initial is None else c(ps0.initial[:13]),
+                     None if ps0.initial is None else c(ps0.g_initial[:13]))
+    fused, params = _make(w, chunk=1500)
+    monkeypatch.setenv("HRKAN_FUSE_SPLIT", "0")
+    plain, _ = _make(w, chunk=1500)
+    monkeypatch.delenv("HRKAN_FUSE_SPLIT")
+    a = _loss_grad_gpu(torch, fused, w, ps)
+    b = _loss_grad_gpu(torch, plain, w, ps)
+    npar = w.num_params()
+    assert rel_l2(a[:npar], b[:npar]) < 1e-5          # same operands; only the bias partial order differs
+    assert abs(a[npar] - b[npar]) <= 1e-6 * abs(b[npar]) and abs(a[npar + 1] - b[npar + 1]) <= 1e-6 * abs(b[npar + 1])
+    _check_loss_grad(a, w, *_loss_grad_oracle(w, params, ps))
+
+
 # ------------------------------------------------------------------ state changes between calls
 def test_engine_switch_after_adam_uses_fresh_tiles(torch_mod):
     """engine 0 (builds the tensor-core weight tiles) -> set_engine(1) -> adam_step -> a call on engine
@@ -255,6 +285,11 @@ def _stress_cases():
         n_bi = int(rng.integers(0, 300))
         chunk = int(rng.integers(1, 4)) * int(rng.integers(97, 1300))
         cases.append((q, D, O_, depth, G, k, m, pde, n_int, n_bi, chunk))
+    # spline orders outside 2..3: k = 1 (two candidate bases), k = 4, 5 (the KT = 8 first-layer table and the
+    # k_last_v2 fallback of the output layer)
+    cases.append((14, 2, 64, 2, 9, 1, 4, "poisson", 1777, 131, 613))
+    cases.append((15, 3, 128, 2, 8, 4, 5, "poisson", 1201, 77, 500))
+    cases.append((16, 2, 256, 2, 7, 5, 6, "burgers", 999, 64, 1024))
     return cases
 
 
