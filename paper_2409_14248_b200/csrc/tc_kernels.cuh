@@ -216,36 +216,37 @@ __global__ void __launch_bounds__(FwdCfg<NF, NS, M, OO>::THREADS, 1)
       } else {
 #pragma unroll 1
       for (int t = 0; t < NMT; ++t) {
+        if (t * 128 + qw * 32 >= O) continue;        // zero-padded rows of a 64-neuron layer: nothing to store
         const int o = t * 128 + qw * 32 + lane;
-        const bool o_ok = o < O;
-        const float b = (sg == 0 && o_ok) ? __ldg(bias + o) : 0.f;
+        const float b = (sg == 0) ? __ldg(bias + o) : 0.f;
         const uint32_t tbase = tmem + ((uint32_t)(qw * 32) << 16) + (uint32_t)((buf * NMT + t) * N);
-        // 16-column chunks are shared round-robin by the generator groups (same lane quadrant)
+        // 16-column chunks are shared round-robin by the generator groups (same lane quadrant); column
+        // col = c*NP + pl -> Y[p0 + pl][c][o] at a 32-bit offset from this lane's base (few live registers)
+        const int lim = (P - p0 < (int64_t)NP) ? (int)(P - p0) : NP;
+        float* yb = Y + p0 * (C * O) + o;
 #pragma unroll 1
         for (int c0 = 16 * grp; c0 < N; c0 += 16 * TC_NGEN) {
           float v[16];
           tc::tmem_ld16(tbase + c0, v);
-          float* yp[16];
-          bool ok[16];
+          if (sg == 0) {
 #pragma unroll
-          for (int q = 0; q < 16; ++q) {
-            const int col = c0 + q;
-            const int c = col / NP, pl = col - c * NP;
-            const int64_t p = p0 + pl;
-            ok[q] = p < P && o_ok;
-            yp[q] = Y + (p * C + c) * (int64_t)O + o;
-            if (sg == 0 && c == 0) v[q] += b;
-          }
-          if (sg > 0) {
+            for (int q = 0; q < 16; ++q)
+              if (c0 + q < NP) v[q] += b;             // value channel c = 0
+          } else {
             float old[16];
 #pragma unroll
-            for (int q = 0; q < 16; ++q) old[q] = ok[q] ? *yp[q] : 0.f;   // 16 loads in flight
+            for (int q = 0; q < 16; ++q) {             // 16 loads in flight
+              const int col = c0 + q, c = col / NP, pl = col - c * NP;
+              old[q] = (pl < lim) ? yb[(pl * C + c) * O] : 0.f;
+            }
 #pragma unroll
             for (int q = 0; q < 16; ++q) v[q] += old[q];
           }
 #pragma unroll
-          for (int q = 0; q < 16; ++q)
-            if (ok[q]) *yp[q] = v[q];
+          for (int q = 0; q < 16; ++q) {
+            const int col = c0 + q, c = col / NP, pl = col - c * NP;
+            if (pl < lim) yb[(pl * C + c) * O] = v[q];
+          }
         }
       }
       }
