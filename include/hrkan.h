@@ -91,6 +91,12 @@ typedef enum {
  * the basis grid range.  Parameters are initialised on `device` with
  * W ~ N(0, 1/(I_l (G+k))) (variance), b = 0 from a counter-based Philox4x32-10 stream keyed by
  * `seed` (SURVEY §8(c) reading 5).  Adam state is zeroed (t = 0).
+ * Execution detail that never shows at this boundary: with at least two hidden layers, every hidden width
+ * in (32, 256] and G+k >= 8, hidden widths other than 64 / 128 / 256 are zero-padded internally to the next
+ * of those so that every hidden->hidden contraction (P:45 / P:87) runs on the tensor-core kernels; padded
+ * neurons have zero weights and bias, emit an all-zero jet and receive a zero adjoint, and every vector
+ * exchanged through this API (parameters, gradient, Adam state) keeps the caller's compact layout for the
+ * widths given here.  Environment HRKAN_PAD_WIDTHS=0 (read at create) disables the padding.
  * EINVAL: n_widths < 2, any width < 1, widths[0] not in {1,2,3}, widths[n-1] != 1, G < 1, k < 1,
  *         m < 2 or m > 8, grid_lo >= grid_hi or non-finite, out == NULL.
  * EUNSUPPORTED: the device is not compute capability 10.0 (sm_100a code only).

@@ -29,8 +29,44 @@ void clear_error() { g_err.clear(); }
 
 namespace {
 
+// Width padding (hrkan_net::padded): one layer of the caller's compact vector <-> the padded layout.
+// dir 0: padded[o][i][n] = compact[o][i][n], padded b[o] = compact b[o] (padding stays zero);
+// dir 1: the reverse gather (gradients).
+__global__ void k_pad_layer(float* __restrict__ cW, float* __restrict__ cb, float* __restrict__ pW,
+                            float* __restrict__ pb, int O, int IB, int IBp, int dir) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t nW = (int64_t)O * IB;
+  if (t >= nW + O) return;
+  float *c, *q;
+  if (t < nW) {
+    const int64_t o = t / IB;
+    c = cW + t;
+    q = pW + o * IBp + (t - o * IB);
+  } else {
+    c = cb + (t - nW);
+    q = pb + (t - nW);
+  }
+  if (dir == 0) *q = *c; else *c = *q;
+}
+
+// hidden width -> the width the tensor-core kernels take (64, 128, 256), or unchanged
+int tc_pad_width(int w) { return w <= 64 ? 64 : w <= 128 ? 128 : 256; }
+
+hrkan_status pad_copy(hrkan_net* net, float* compact, float* padded, int dir, cudaStream_t st) {
+  for (int l = 0; l < net->L; ++l) {
+    const int O = net->pub_widths[l + 1], IB = net->pub_widths[l] * net->B, IBp = net->widths[l] * net->B;
+    const int64_t n = (int64_t)O * IB + O;
+    HR_LAUNCH(HRKAN_K_OTHER, "k_pad_layer",
+              k_pad_layer<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
+                  compact + net->pub_w_off[l], compact + net->pub_b_off[l], padded + net->w_off[l],
+                  padded + net->b_off[l], O, IB, IBp, dir));
+  }
+  return HRKAN_OK;
+}
+
 hrkan_status refresh_derived(hrkan_net* net, cudaStream_t st, bool force = false) {
   if (!net->derived_dirty && !force) return HRKAN_OK;
+  if (net->padded) HR_TRY(pad_copy(net, net->pub_params, net->params, 0, st));
   for (int l = 0; l < net->L; ++l) {
     const int I = net->widths[l], O = net->widths[l + 1];
     const int64_t n = (int64_t)O * I * net->B;
@@ -142,7 +178,8 @@ hrkan_status hrkan_create(const int32_t* widths, int32_t n_widths, int32_t G, in
   hrkan_net* net = new hrkan_net();
   net->device = device;
   net->num_sms = prop.multiProcessorCount;
-  net->widths.assign(widths, widths + n_widths);
+  net->pub_widths.assign(widths, widths + n_widths);
+  net->widths = net->pub_widths;
   net->L = n_widths - 1;
   net->D = widths[0];
   net->G = G;
@@ -159,17 +196,37 @@ hrkan_status hrkan_create(const int32_t* widths, int32_t n_widths, int32_t G, in
   net->bc.mid0 = (float)(grid_lo + 0.5 * (1 - k) * h);
   net->bc.k = k;
   net->bc.B = G + k;
-  int64_t off = 0;
+  // Width padding: with at least two hidden layers, every hidden width in (32, 256] and B >= 8 (the
+  // tensor-core conditions of tc_layer_ok), hidden widths are zero-padded to 64 / 128 / 256 so that
+  // every hidden->hidden layer runs on the tensor cores (HRKAN_PAD_WIDTHS=0 disables it).
+  {
+    bool pad_ok = n_widths >= 4 && net->B >= 8, any = false;
+    if (const char* e = std::getenv("HRKAN_PAD_WIDTHS")) pad_ok = pad_ok && std::atoi(e) != 0;
+    for (int i = 1; i + 1 < n_widths; ++i) {
+      pad_ok = pad_ok && widths[i] > 32 && widths[i] <= 256;
+      any = any || tc_pad_width(widths[i]) != widths[i];
+    }
+    if (pad_ok && any) {
+      net->padded = true;
+      for (int i = 1; i + 1 < n_widths; ++i) net->widths[i] = tc_pad_width(widths[i]);
+    }
+  }
+  int64_t off = 0, poff = 0;
   for (int l = 0; l < net->L; ++l) {
-    const int64_t nW = (int64_t)widths[l + 1] * widths[l] * net->B;
+    const int64_t nW = (int64_t)net->widths[l + 1] * net->widths[l] * net->B;
     net->w_off.push_back(off);
     off += nW;
     net->b_off.push_back(off);
-    off += widths[l + 1];
+    off += net->widths[l + 1];
     net->max_layer_w = std::max(net->max_layer_w, nW);
-    net->max_width = std::max(net->max_width, widths[l + 1]);
+    net->max_width = std::max(net->max_width, net->widths[l + 1]);
+    net->pub_w_off.push_back(poff);
+    poff += (int64_t)widths[l + 1] * widths[l] * net->B;
+    net->pub_b_off.push_back(poff);
+    poff += widths[l + 1];
   }
   net->n_params = off;
+  net->pub_n_params = poff;
   // tuning overrides for experiments (precision/speed trade-off of the TMEM drain segments)
   if (const char* e = std::getenv("HRKAN_TC_SEG")) net->tc_seg = net->tc_seg_single = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("HRKAN_TC_WSEG")) net->tc_wseg = std::max(1, std::atoi(e));
@@ -180,15 +237,24 @@ hrkan_status hrkan_create(const int32_t* widths, int32_t n_widths, int32_t G, in
     return s;
   };
   if (cudaMalloc(&net->params, sizeof(float) * off) != cudaSuccess ||
-      cudaMalloc(&net->adam_m, sizeof(float) * off) != cudaSuccess ||
-      cudaMalloc(&net->adam_v, sizeof(float) * off) != cudaSuccess ||
+      cudaMalloc(&net->adam_m, sizeof(float) * poff) != cudaSuccess ||
+      cudaMalloc(&net->adam_v, sizeof(float) * poff) != cudaSuccess ||
       cudaMalloc(&net->adam_t, 2 * sizeof(int)) != cudaSuccess) {
     cudaGetLastError();
     return cleanup(fail(HRKAN_ENOMEM, "parameter allocation failed"));
   }
+  net->pub_params = net->params;
+  if (net->padded) {
+    net->pub_params = nullptr;
+    if (cudaMalloc(&net->pub_params, sizeof(float) * poff) != cudaSuccess ||
+        cudaMemset(net->params, 0, sizeof(float) * off) != cudaSuccess) {   // the padding stays zero for good
+      cudaGetLastError();
+      return cleanup(fail(HRKAN_ENOMEM, "parameter allocation failed"));
+    }
+  }
   net->wt.assign(net->L, nullptr);
   for (int l = 0; l < net->L; ++l) {
-    if (cudaMalloc(&net->wt[l], sizeof(float) * (size_t)widths[l + 1] * widths[l] * net->B) != cudaSuccess) {
+    if (cudaMalloc(&net->wt[l], sizeof(float) * (size_t)net->widths[l + 1] * net->widths[l] * net->B) != cudaSuccess) {
       cudaGetLastError();
       return cleanup(fail(HRKAN_ENOMEM, "weight copy allocation failed"));
     }
@@ -200,7 +266,7 @@ hrkan_status hrkan_create(const int32_t* widths, int32_t n_widths, int32_t G, in
   return HRKAN_OK;
 }
 
-int64_t hrkan_num_params(hrkan_net_t net) { return net ? net->n_params : -1; }
+int64_t hrkan_num_params(hrkan_net_t net) { return net ? net->pub_n_params : -1; }
 
 int64_t hrkan_launch_count(hrkan_net_t net) { return net ? net->launches : -1; }
 
@@ -226,16 +292,17 @@ hrkan_status hrkan_init_params(hrkan_net_t net, uint64_t seed, void* stream) {
   DeviceGuard dg(net->device);
   cudaStream_t st = (cudaStream_t)stream;
   for (int l = 0; l < net->L; ++l) {
-    const int I = net->widths[l], O = net->widths[l + 1];
+    const int I = net->pub_widths[l], O = net->pub_widths[l + 1];     // the caller's (unpadded) layer
     const int64_t nW = (int64_t)O * I * net->B;
     const float stdv = (float)(1.0 / std::sqrt((double)I * net->B));
     const int64_t n = std::max<int64_t>(nW, O);
-    k_init_layer<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(net->params + net->w_off[l], net->params + net->b_off[l], nW, O,
-                                                              stdv, seed, (uint32_t)l);
+    k_init_layer<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(net->pub_params + net->pub_w_off[l],
+                                                              net->pub_params + net->pub_b_off[l], nW, O, stdv, seed,
+                                                              (uint32_t)l);
     HR_TRY(check_launch(net, "k_init_layer"));
   }
-  HR_CUDA(cudaMemsetAsync(net->adam_m, 0, sizeof(float) * net->n_params, st));
-  HR_CUDA(cudaMemsetAsync(net->adam_v, 0, sizeof(float) * net->n_params, st));
+  HR_CUDA(cudaMemsetAsync(net->adam_m, 0, sizeof(float) * net->pub_n_params, st));
+  HR_CUDA(cudaMemsetAsync(net->adam_v, 0, sizeof(float) * net->pub_n_params, st));
   HR_CUDA(cudaMemsetAsync(net->adam_t, 0, 2 * sizeof(int), st));
   net->derived_dirty = true;
   return HRKAN_OK;
@@ -244,14 +311,14 @@ hrkan_status hrkan_init_params(hrkan_net_t net, uint64_t seed, void* stream) {
 hrkan_status hrkan_get_params(hrkan_net_t net, float* dst, void* stream) {
   if (!net || !dst) return fail(HRKAN_EINVAL, "NULL argument");
   DeviceGuard dg(net->device);
-  HR_CUDA(cudaMemcpyAsync(dst, net->params, sizeof(float) * net->n_params, cudaMemcpyDefault, (cudaStream_t)stream));
+  HR_CUDA(cudaMemcpyAsync(dst, net->pub_params, sizeof(float) * net->pub_n_params, cudaMemcpyDefault, (cudaStream_t)stream));
   return HRKAN_OK;
 }
 
 hrkan_status hrkan_set_params(hrkan_net_t net, const float* src, void* stream) {
   if (!net || !src) return fail(HRKAN_EINVAL, "NULL argument");
   DeviceGuard dg(net->device);
-  HR_CUDA(cudaMemcpyAsync(net->params, src, sizeof(float) * net->n_params, cudaMemcpyDefault, (cudaStream_t)stream));
+  HR_CUDA(cudaMemcpyAsync(net->pub_params, src, sizeof(float) * net->pub_n_params, cudaMemcpyDefault, (cudaStream_t)stream));
   net->derived_dirty = true;
   return HRKAN_OK;
 }
@@ -334,7 +401,8 @@ hrkan_status loss_grad_body(hrkan_net* net, const hrkan_pde* pde, const float* i
                             const float* initial, const float* g_initial, int64_t N0, int64_t Ni_global,
                             int64_t Nbi_global, float* out, cudaStream_t st, bool force_refresh) {
   const int D = net->D;
-  const int64_t np = net->n_params;
+  const int64_t np = net->n_params;        // gradient length of the net the kernels run on (padded or not)
+  const int64_t pnp = net->pub_n_params;   // the caller's vector: [dθ (pnp) | aL_pde | L_bi | flag | pad]
   const float *d_int, *d_f = nullptr, *d_bnd, *d_gb, *d_ini, *d_gi;
   HR_TRY(stage_in(interior, Ni * D, net->st_int, st, &d_int));
   if (forcing && (pde->kind == HRKAN_POISSON || pde->kind == HRKAN_ANISO)) HR_TRY(stage_in(forcing, Ni, net->st_f, st, &d_f));
@@ -345,14 +413,19 @@ hrkan_status loss_grad_body(hrkan_net* net, const hrkan_pde* pde, const float* i
   float* dout = out;
   const bool host_out = !is_device_ptr(out);
   if (host_out) {
-    HR_CUDA(net->st_out.ensure(sizeof(float) * (np + 4)));
+    HR_CUDA(net->st_out.ensure(sizeof(float) * (pnp + 4)));
     dout = net->st_out.f();
+  }
+  float* const cout_ = dout;               // compact result (device)
+  if (net->padded) {                        // the passes accumulate into the padded layout, gathered at the end
+    HR_CUDA(net->pad_grad.ensure(sizeof(float) * (np + 4)));
+    dout = net->pad_grad.f();
   }
   if (tiny_eligible(net) && (pde->kind == HRKAN_POISSON || pde->kind == HRKAN_BURGERS)) {
     TinyArgs t{pde, d_int, d_f, d_bnd, d_gb, d_ini, d_gi, Ni, Nb, N0, (float)(1.0 / (double)std::max<int64_t>(1, Ni_global)),
                Nbi_global > 0 ? (float)(1.0 / (double)Nbi_global) : 0.f, dout};
     HR_TRY(tiny_step(net, t, st));
-    if (host_out) HR_CUDA(cudaMemcpyAsync(out, dout, sizeof(float) * (np + 4), cudaMemcpyDeviceToHost, st));
+    if (host_out) HR_CUDA(cudaMemcpyAsync(out, dout, sizeof(float) * (pnp + 4), cudaMemcpyDeviceToHost, st));
     return HRKAN_OK;
   }
   HR_CUDA(cudaMemsetAsync(dout, 0, sizeof(float) * (np + 4), st));
@@ -393,7 +466,11 @@ hrkan_status loss_grad_body(hrkan_net* net, const hrkan_pde* pde, const float* i
     a.g = d_gi;
     HR_TRY(dispatch_pass(net, 0, 0, a, st));
   }
-  if (host_out) HR_CUDA(cudaMemcpyAsync(out, dout, sizeof(float) * (np + 4), cudaMemcpyDeviceToHost, st));
+  if (net->padded) {
+    HR_TRY(pad_copy(net, cout_, dout, 1, st));
+    HR_CUDA(cudaMemcpyAsync(cout_ + pnp, dout + np, 4 * sizeof(float), cudaMemcpyDeviceToDevice, st));
+  }
+  if (host_out) HR_CUDA(cudaMemcpyAsync(out, cout_, sizeof(float) * (pnp + 4), cudaMemcpyDeviceToHost, st));
   return HRKAN_OK;
 }
 
@@ -516,10 +593,10 @@ hrkan_status hrkan_adam_step(hrkan_net_t net, const float* grad, float lr, float
   DeviceGuard dg(net->device);
   cudaStream_t st = (cudaStream_t)stream;
   const float* dg_ptr;
-  HR_TRY(stage_in(grad, net->n_params, net->st_out, st, &dg_ptr));
-  const int64_t n = net->n_params;
+  HR_TRY(stage_in(grad, net->pub_n_params, net->st_out, st, &dg_ptr));
+  const int64_t n = net->pub_n_params;
   HR_LAUNCH(HRKAN_K_ADAM, "k_adam",
-            k_adam<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(net->params, net->adam_m, net->adam_v, dg_ptr, n, lr, beta1,
+            k_adam<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(net->pub_params, net->adam_m, net->adam_v, dg_ptr, n, lr, beta1,
                                                                 beta2, eps, net->adam_t));
   net->derived_dirty = true;
   return HRKAN_OK;
@@ -561,6 +638,7 @@ void hrkan_free(hrkan_net_t net) {
     cudaEventDestroy(ev.a);
     cudaEventDestroy(ev.b);
   }
+  if (net->pub_params != net->params) cudaFree(net->pub_params);
   cudaFree(net->params);
   cudaFree(net->adam_m);
   cudaFree(net->adam_v);
@@ -569,7 +647,7 @@ void hrkan_free(hrkan_net_t net) {
   DevBuf* bufs[] = {&net->jets, &net->adj_a, &net->adj_b, &net->loss_part, &net->w_part, &net->b_part, &net->last_part, &net->first_part,
                     &net->st_int, &net->st_f, &net->st_bnd, &net->st_gb, &net->st_ini, &net->st_gi,
                     &net->st_out, &net->st_pts, &net->st_u, &net->st_du, &net->st_d2u, &net->tc_ws,
-                    &net->tc_yw, &net->tc_yd, &net->tiny_cnt};
+                    &net->tc_yw, &net->tc_yd, &net->tiny_cnt, &net->pad_grad, &net->tc_bias_part};
   for (DevBuf* b : bufs) b->release();
   tc_free(net);
   delete net;

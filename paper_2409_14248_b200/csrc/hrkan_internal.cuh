@@ -123,7 +123,18 @@ struct hrkan_net {
   int64_t max_layer_w = 0;
   int max_width = 0;                   // max over widths[1..L]
   BasisCfg bc{};
-  float* params = nullptr;             // flat, owned
+  float* params = nullptr;             // flat, owned (the layout the kernels run on: `widths`)
+  // Width padding (hrkan_create): hidden widths in (32, 256] that the tensor-core kernels do not take
+  // (they need 64, 128 or 256 neurons) are zero-padded up to the next such width.  `widths`, `w_off`,
+  // `b_off`, `n_params` and `params` then describe the padded net the kernels run on; the public
+  // parameter / gradient vectors keep the caller's compact layout (`pub_*`), which is also the Adam
+  // master copy.  Padded neurons have zero weights and bias, so they emit an all-zero jet and receive a
+  // zero adjoint: the compact entries of every result are unchanged.  Not padded: pub_params == params.
+  bool padded = false;
+  std::vector<int> pub_widths;
+  std::vector<int64_t> pub_w_off, pub_b_off;
+  int64_t pub_n_params = 0;
+  float* pub_params = nullptr;
   float* adam_m = nullptr;
   float* adam_v = nullptr;
   int* adam_t = nullptr;               // device [t, finished-block counter]: k_adam increments t on the
@@ -140,6 +151,7 @@ struct hrkan_net {
   DevBuf tc_ws;                         // tensor-core path scratch
   DevBuf tiny_cnt;                      // k_tiny_step's finished-block counter (reset by the last block)
   DevBuf tc_yw, tc_yd;                  // pre-split bf16 hi/lo Ybar operands of the reverse kernels
+  DevBuf pad_grad;                      // [n_params + 4] gradient of the padded net (gathered into the caller's compact vector)
   DevBuf tc_bias_part;                  // bias-gradient partials emitted by the fused output layer (k_last_v3 SPLIT)
   std::vector<TcLayerState> tc_layers;
   int tc_seg = 96;                      // K-blocks per forward TMEM segment, double-buffered accumulators (C3/C4: one segment;

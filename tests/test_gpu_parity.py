@@ -88,11 +88,25 @@ def _loss_grad_gpu(torch, net, w, ps, **kw):
     return out.cpu().numpy()
 
 
+_ORACLE_CACHE = {}
+
+
 def _loss_grad_oracle(w, params, ps, **kw):
+    """The float64 oracle on (w, params, ps); memoised on the CONTENT of its inputs, so tests that put
+    different kernel configurations through the same seeded inputs (the multi-segment wgrad tests, the
+    m sweep) pay for the CPU oracle once per distinct input."""
+    import hashlib
     bi = ps.boundary if ps.initial is None else np.concatenate([ps.boundary, ps.initial])
     gbi = ps.g_boundary if ps.initial is None else np.concatenate([ps.g_boundary, ps.g_initial])
-    lp, lb, g = O.loss_grad(_oracle_net(w), params, _pde(w), ps.interior, bi, gbi, **kw)
-    return lp, lb, g
+    h = hashlib.sha1(repr((tuple(w.widths), w.G, w.k, w.m, w.lo, w.hi, sorted(_pde(w).items()), sorted(kw.items()))).encode())
+    for a in [ps.interior, bi, gbi] + [x for Wb in params for x in Wb]:
+        a = np.ascontiguousarray(a)
+        h.update(repr((a.shape, a.dtype.str)).encode())
+        h.update(a.tobytes())
+    key = h.hexdigest()
+    if key not in _ORACLE_CACHE:
+        _ORACLE_CACHE[key] = O.loss_grad(_oracle_net(w), params, _pde(w), ps.interior, bi, gbi, **kw)
+    return _ORACLE_CACHE[key]
 
 
 def _check_loss_grad(out, w, lp, lb, g):
