@@ -105,6 +105,14 @@ hrkan_status hrkan_create(const int32_t* widths, int32_t n_widths, int32_t G, in
                           float grid_lo, float grid_hi, uint64_t seed, int32_t device,
                           hrkan_net_t* out);
 
+/* The widths the kernels of a net created with these arguments run on (host-only query, no device
+ * needed): `out[0..n_widths-1]` (host) receives `widths` with the hidden entries zero-padded as
+ * hrkan_create's "execution detail" describes (equal to `widths` when no padding applies or
+ * HRKAN_PAD_WIDTHS=0).  The public vectors never use these widths; the query exists so that callers
+ * and tests can see which nets take the tensor-core path.  EINVAL: NULL pointers, n_widths < 2,
+ * a width < 1, G < 1 or k < 1. */
+hrkan_status hrkan_execution_widths(const int32_t* widths, int32_t n_widths, int32_t G, int32_t k, int32_t* out);
+
 /* Number of parameters = sum_l O_l*I_l*(G+k) + O_l.  Returns -1 for a NULL net. */
 int64_t hrkan_num_params(hrkan_net_t net);
 

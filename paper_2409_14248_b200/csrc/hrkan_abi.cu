@@ -52,6 +52,23 @@ __global__ void k_pad_layer(float* __restrict__ cW, float* __restrict__ cb, floa
 // hidden width -> the width the tensor-core kernels take (64, 128, 256), or unchanged
 int tc_pad_width(int w) { return w <= 64 ? 64 : w <= 128 ? 128 : 256; }
 
+// The widths the kernels run on (see hrkan_net::padded): with at least two hidden layers, every hidden
+// width in (32, 256] and B >= 8 (the tensor-core conditions of tc_layer_ok), hidden widths are
+// zero-padded to 64 / 128 / 256 so that every hidden->hidden layer runs on the tensor cores
+// (HRKAN_PAD_WIDTHS=0 disables it).  Returns whether any width changed.
+bool execution_widths(const int32_t* widths, int n_widths, int B, std::vector<int>& out) {
+  out.assign(widths, widths + n_widths);
+  bool pad_ok = n_widths >= 4 && B >= 8, any = false;
+  if (const char* e = std::getenv("HRKAN_PAD_WIDTHS")) pad_ok = pad_ok && std::atoi(e) != 0;
+  for (int i = 1; i + 1 < n_widths; ++i) {
+    pad_ok = pad_ok && widths[i] > 32 && widths[i] <= 256;
+    any = any || tc_pad_width(widths[i]) != widths[i];
+  }
+  if (!(pad_ok && any)) return false;
+  for (int i = 1; i + 1 < n_widths; ++i) out[i] = tc_pad_width(widths[i]);
+  return true;
+}
+
 hrkan_status pad_copy(hrkan_net* net, float* compact, float* padded, int dir, cudaStream_t st) {
   for (int l = 0; l < net->L; ++l) {
     const int O = net->pub_widths[l + 1], IB = net->pub_widths[l] * net->B, IBp = net->widths[l] * net->B;
@@ -196,21 +213,7 @@ hrkan_status hrkan_create(const int32_t* widths, int32_t n_widths, int32_t G, in
   net->bc.mid0 = (float)(grid_lo + 0.5 * (1 - k) * h);
   net->bc.k = k;
   net->bc.B = G + k;
-  // Width padding: with at least two hidden layers, every hidden width in (32, 256] and B >= 8 (the
-  // tensor-core conditions of tc_layer_ok), hidden widths are zero-padded to 64 / 128 / 256 so that
-  // every hidden->hidden layer runs on the tensor cores (HRKAN_PAD_WIDTHS=0 disables it).
-  {
-    bool pad_ok = n_widths >= 4 && net->B >= 8, any = false;
-    if (const char* e = std::getenv("HRKAN_PAD_WIDTHS")) pad_ok = pad_ok && std::atoi(e) != 0;
-    for (int i = 1; i + 1 < n_widths; ++i) {
-      pad_ok = pad_ok && widths[i] > 32 && widths[i] <= 256;
-      any = any || tc_pad_width(widths[i]) != widths[i];
-    }
-    if (pad_ok && any) {
-      net->padded = true;
-      for (int i = 1; i + 1 < n_widths; ++i) net->widths[i] = tc_pad_width(widths[i]);
-    }
-  }
+  net->padded = execution_widths(widths, n_widths, net->B, net->widths);
   int64_t off = 0, poff = 0;
   for (int l = 0; l < net->L; ++l) {
     const int64_t nW = (int64_t)net->widths[l + 1] * net->widths[l] * net->B;
@@ -263,6 +266,17 @@ hrkan_status hrkan_create(const int32_t* widths, int32_t n_widths, int32_t G, in
   if (s != HRKAN_OK) return cleanup(s);
   if (cudaDeviceSynchronize() != cudaSuccess) return cleanup(fail(HRKAN_ECUDA, "init failed"));
   *out = net;
+  return HRKAN_OK;
+}
+
+hrkan_status hrkan_execution_widths(const int32_t* widths, int32_t n_widths, int32_t G, int32_t k, int32_t* out) {
+  if (!widths || !out || n_widths < 2) return fail(HRKAN_EINVAL, "NULL argument or fewer than 2 widths");
+  if (G < 1 || k < 1) return fail(HRKAN_EINVAL, "G and k must be >= 1");
+  for (int i = 0; i < n_widths; ++i)
+    if (widths[i] < 1) return fail(HRKAN_EINVAL, "widths must be >= 1");
+  std::vector<int> w;
+  execution_widths(widths, n_widths, G + k, w);
+  for (int i = 0; i < n_widths; ++i) out[i] = w[i];
   return HRKAN_OK;
 }
 

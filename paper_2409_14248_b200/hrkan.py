@@ -35,6 +35,7 @@ _P = ctypes.c_void_p
 _I32, _I64, _F, _U64 = ctypes.c_int32, ctypes.c_int64, ctypes.c_float, ctypes.c_uint64
 SYMBOLS = [
     ("hrkan_create", ctypes.c_int, [ctypes.POINTER(_I32), _I32, _I32, _I32, _I32, _F, _F, _U64, _I32, ctypes.POINTER(_P)]),
+    ("hrkan_execution_widths", ctypes.c_int, [ctypes.POINTER(_I32), _I32, _I32, _I32, ctypes.POINTER(_I32)]),
     ("hrkan_num_params", _I64, [_P]),
     ("hrkan_get_params", ctypes.c_int, [_P, _P, _P]),
     ("hrkan_set_params", ctypes.c_int, [_P, _P, _P]),

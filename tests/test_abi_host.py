@@ -79,3 +79,33 @@ def test_invalid_arguments_rejected_without_device():
     pde = hrkan.pde_struct("poisson")
     assert lib.hrkan_pinn_loss_grad(None, ctypes.byref(pde), None, None, 0, None, None, 0, None, None, 0,
                                     0, 0, None, None) == EINVAL
+
+
+def test_execution_widths_padding_rule(monkeypatch):
+    """hrkan_execution_widths (host-only): hidden widths in (32, 256] are padded to 64 / 128 / 256 when the
+    net has at least two hidden layers, all in that range, and G + k >= 8; otherwise unchanged."""
+    lib = _lib()
+
+    def ew(widths, G=10, k=3):
+        w = (ctypes.c_int32 * len(widths))(*widths)
+        out = (ctypes.c_int32 * len(widths))()
+        assert lib.hrkan_execution_widths(w, len(widths), G, k, out) == 0
+        return list(out)
+
+    assert ew([2, 100, 100, 1]) == [2, 128, 128, 1]
+    assert ew([2, 48, 200, 72, 1]) == [2, 64, 256, 128, 1]
+    assert ew([3, 33, 256, 1]) == [3, 64, 256, 1]
+    assert ew([2, 64, 64, 1]) == [2, 64, 64, 1]                   # already tensor-core widths
+    assert ew([2, 100, 1]) == [2, 100, 1]                         # one hidden layer: no hidden->hidden contraction
+    assert ew([2, 100, 20, 1]) == [2, 100, 20, 1]                 # a thin hidden layer keeps the SIMT engine
+    assert ew([2, 100, 300, 1]) == [2, 100, 300, 1]               # wider than the tensor-core kernels take
+    assert ew([2, 5, 5, 1]) == [2, 5, 5, 1]                       # tiny nets: the one-launch kernel
+    assert ew([2, 100, 100, 1], G=3, k=3) == [2, 100, 100, 1]     # G + k < 8: no tensor-core path
+    monkeypatch.setenv("HRKAN_PAD_WIDTHS", "0")
+    assert ew([2, 100, 100, 1]) == [2, 100, 100, 1]
+    monkeypatch.delenv("HRKAN_PAD_WIDTHS")
+    out = (ctypes.c_int32 * 2)()
+    assert lib.hrkan_execution_widths(None, 2, 5, 3, out) == 1
+    w = (ctypes.c_int32 * 2)(2, 1)
+    assert lib.hrkan_execution_widths(w, 1, 5, 3, out) == 1
+    assert lib.hrkan_execution_widths(w, 2, 0, 3, out) == 1
