@@ -356,7 +356,7 @@ __global__ void __launch_bounds__(FL_THREADS) k_wgrad_first_r(const float* __res
   extern __shared__ __align__(16) float wsm[];
   const int B = bc.B;
   const int QG = (int)blockDim.x / O;
-  const int ring = max(2 * PB * C * O, QG * D * B * O);
+  const int ring = (max(2 * PB * C * O, QG * D * B * O) + 3) & ~3;   // the table after it stays 16-B aligned
   float* ybs = wsm;                               // [2][PB][C][O] adjoint rows (bulk copies, 2-stage ring);
                                                   // at the end [QG][D*B][O] accumulators
   float* V = ybs + ring;                          // [PB][D][3][BMAX]
@@ -448,6 +448,183 @@ __global__ void __launch_bounds__(FL_THREADS) k_wgrad_first_r(const float* __res
       }
     }
     __syncthreads();                              // stage b & 1 fully read
+    if (threadIdx.x == 0 && b + 2 < nbat) {
+      tc::fence_proxy_async_smem();               // generic reads of the stage before the async-proxy refill
+      issue(b + 2);
+    }
+  }
+  // fixed-order sum over the point groups: accumulators -> shared [QG][D*B][O] (the stage ring is free now)
+  const int64_t nW = (int64_t)O * D * B;
+  float* dst = part + (int64_t)blockIdx.x * nW;
+  float* accs = ybs;
+  __syncthreads();
+  if (active) {
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+#pragma unroll
+      for (int j = 0; j < NPR; ++j) {
+        float lo_, hi_;
+        tc::upk2(acc[a][j], lo_, hi_);
+        if (2 * j < B) accs[((qg * D + a) * B + 2 * j) * O + o] = lo_;
+        if (2 * j + 1 < B) accs[((qg * D + a) * B + 2 * j + 1) * O + o] = hi_;
+      }
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < D * B * O; e += blockDim.x) {
+    float v = 0.f;
+    for (int g = 0; g < QG; ++g) v += accs[g * D * B * O + e];
+    const int oo = e % O, an = e / O;            // accs index (a*B + n)*O + o
+    dst[(int64_t)oo * D * B + an] = v;
+  }
+  __syncthreads();
+  red[threadIdx.x] = active ? dbs : 0.f;
+  __syncthreads();
+  if (qg == 0) {
+    float v = 0.f;
+    for (int g = 0; g < QG; ++g) v += red[g * O + o];
+    part_b[blockIdx.x * (int64_t)O + o] = v;
+  }
+}
+
+
+// Band-limited variant of k_wgrad_first_r for k <= 3 (HRKAN_WF_WINDOW, default on): every thread of the block
+// works on the SAME point, so the k+1 <= 4 non-zero bases of a coordinate sit at a block-uniform position --
+// the update touches only the three accumulator pairs jp .. jp+2 (jp = floor(n0 / 2) clamped into the
+// table, which covers n0 .. n0+3 and every in-range basis of an out-of-grid x) through a block-uniform
+// switch over jp, 9 FFMA2 per coordinate instead of 3 * BMAX/2.  The per-batch table holds v, v', v'' of
+// those six bases only and is double-buffered: batch b+1's table is built by the first threads while the
+// block accumulates batch b (one __syncthreads per batch).
+#ifndef HRKAN_WF_WINDOW
+#define HRKAN_WF_WINDOW 1
+#endif
+// f(integral_constant<J>) for the block-uniform J = jp in [0, NPR-3] (NPR <= 10: at most 8 cases)
+template <int NPR, class F>
+__device__ __forceinline__ void wf_switch(int jp, F&& f) {
+  static_assert(NPR - 3 <= 7, "extend the switch");
+#define HRKAN_WF_CASE(J)                                                    \
+  case J:                                                                   \
+    if constexpr (J <= NPR - 3) f(std::integral_constant<int, J>{});        \
+    break;
+  switch (jp) {
+    HRKAN_WF_CASE(0) HRKAN_WF_CASE(1) HRKAN_WF_CASE(2) HRKAN_WF_CASE(3)
+    HRKAN_WF_CASE(4) HRKAN_WF_CASE(5) HRKAN_WF_CASE(6) HRKAN_WF_CASE(7)
+  }
+#undef HRKAN_WF_CASE
+}
+
+template <int NF, int NS, int M, int BMAX>
+__global__ void __launch_bounds__(FL_THREADS) k_wgrad_first_w(const float* __restrict__ pts,
+                                                              const float* __restrict__ Ybar, float* __restrict__ part,
+                                                              float* __restrict__ part_b, int64_t P, int O,
+                                                              BasisCfg bc) {
+  constexpr int D = NF;
+  constexpr int C = 1 + NF + NS;
+  constexpr int NPR = BMAX / 2;                   // accumulator pairs per coordinate
+  constexpr int TW = 3 * 6 + 2;                   // table row: [3 orders][6 bases] + jp + pad (8-B aligned)
+  static_assert(NPR >= 3, "window of three pairs");
+  const int PB = wf_pb(C, O);
+  extern __shared__ __align__(16) float wsm[];
+  const int B = bc.B;
+  const int QG = (int)blockDim.x / O;
+  const int ring = (max(2 * PB * C * O, QG * D * B * O) + 3) & ~3;   // the table after it stays 16-B aligned
+  float* ybs = wsm;                               // [2][PB][C][O] adjoint rows (bulk copies, 2-stage ring);
+                                                  // at the end [QG][D*B][O] accumulators
+  float* V = ybs + ring;                          // [2][PB][D][TW]
+  float* red = V + 2 * PB * D * TW;               // [FL_THREADS] fixed-order point-group reduction
+  __shared__ __align__(8) uint64_t full[2];
+  const int qg = (int)threadIdx.x / O, o = (int)threadIdx.x % O;
+  const bool active = qg < QG;
+  uint64_t acc[D][NPR];
+#pragma unroll
+  for (int a = 0; a < D; ++a)
+#pragma unroll
+    for (int j = 0; j < NPR; ++j) acc[a][j] = 0ull;   // (0.f, 0.f)
+  float dbs = 0.f;
+  const int64_t lo = (P * blockIdx.x) / gridDim.x, hi = (P * (blockIdx.x + 1)) / gridDim.x;
+  const int nbat = (int)((hi - lo + PB - 1) / PB);
+  const uint32_t row_bytes = (uint32_t)(C * O * 4);
+  auto issue = [&](int b) {                       // thread 0: batch b -> stage b & 1
+    const int64_t p0 = lo + (int64_t)b * PB;
+    const int npb = (int)((hi - p0) < PB ? (hi - p0) : PB);
+    tc::mbar_arrive_expect_tx(&full[b & 1], row_bytes * npb);
+    tc::bulk_g2s(ybs + (b & 1) * (PB * C * O), Ybar + p0 * (int64_t)(C * O), row_bytes * npb, &full[b & 1]);
+  };
+  // table of batch b: task = (point q, coordinate a, basis u of the six 2 jp .. 2 jp + 5), spread over the
+  // warps (lanes 0 .. NTL-1 of each) so that no single warp carries the build
+  const int warp_ = (int)threadIdx.x >> 5, lane_ = (int)threadIdx.x & 31, nwarp_ = (int)blockDim.x >> 5;
+  const int ntask = PB * D * 6, NTL = (ntask + nwarp_ - 1) / nwarp_;
+  auto build = [&](int b) {
+    const int64_t p0 = lo + (int64_t)b * PB;
+    const int nq = (int)((hi - p0) < PB ? (hi - p0) : PB);
+    for (int l = lane_; l < NTL; l += 32) {
+      const int e6 = warp_ * NTL + l;
+      if (e6 >= ntask) break;
+      const int e = e6 / 6, u = e6 - e * 6;
+      const int q = e / D;
+      float* row = V + ((b & 1) * PB * D + e) * TW;
+      const float x = (q < nq) ? __ldg(pts + (p0 + q) * D + (e - q * D)) : 0.f;
+      int jp = first_basis(x, bc) >> 1;           // floor(n0 / 2), also for negative n0
+      jp = min(max(jp, 0), NPR - 3);
+      const int n = 2 * jp + u;
+      float v0 = 0.f, v1 = 0.f, v2 = 0.f, v3;
+      if (q < nq && n < B) hr_eval<M, (NS > 0 ? 2 : 1)>(basis_q(x, n, bc), bc.sc, v0, v1, v2, v3);
+      if (q < nq && x != x) v0 = v1 = v2 = x;     // NaN inputs poison their row (flagged downstream)
+      row[u] = v0;
+      row[6 + u] = v1;
+      row[12 + u] = v2;
+      if (u == 0) reinterpret_cast<int*>(row)[18] = jp;
+    }
+  };
+  if (threadIdx.x == 0) {
+    tc::mbar_init(&full[0], 1);
+    tc::mbar_init(&full[1], 1);
+    tc::fence_mbar_init();
+    if (nbat > 0) issue(0);
+    if (nbat > 1) issue(1);
+  }
+  if (nbat > 0) build(0);
+  __syncthreads();                                // barrier init and table 0 visible
+  for (int b = 0; b < nbat; ++b) {
+    const int64_t p0 = lo + (int64_t)b * PB;
+    const int nq = (int)((hi - p0) < PB ? (hi - p0) : PB);
+    if (b + 1 < nbat) build(b + 1);               // other half of the table ring (batch b-1 finished at the last barrier)
+    tc::mbar_wait(&full[b & 1], (uint32_t)((b >> 1) & 1));
+    const float* yst = ybs + (b & 1) * (PB * C * O) + o;
+    const float* Vb = V + (b & 1) * PB * D * TW;
+    if (active) {
+      for (int q = qg; q < nq; q += QG) {
+        float y[C];
+#pragma unroll
+        for (int c = 0; c < C; ++c) y[c] = yst[(q * C + c) * O];
+        dbs += y[0];
+        const uint64_t Y0 = tc::pk2(y[0], y[0]);
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+          const uint64_t Y1 = tc::pk2(y[1 + a], y[1 + a]);
+          const float y2 = (a < NS) ? y[1 + NF + (a < NS ? a : 0)] : 0.f;
+          const uint64_t Y2 = tc::pk2(y2, y2);
+          const float* row = Vb + (q * D + a) * TW;
+          // the point's contribution to the three pairs (independent of the accumulators: full ILP) ...
+          uint64_t c3[3];
+#pragma unroll
+          for (int w = 0; w < 3; ++w) {
+            uint64_t t = tc::mul2(Y1, *reinterpret_cast<const uint64_t*>(row + 6 + 2 * w));
+            if (a < NS) t = tc::fma2(Y2, *reinterpret_cast<const uint64_t*>(row + 12 + 2 * w), t);
+            c3[w] = tc::fma2(Y0, *reinterpret_cast<const uint64_t*>(row + 2 * w), t);
+          }
+          // ... added to the accumulator pairs jp .. jp+2 (block-uniform jp)
+          const int jp = reinterpret_cast<const int*>(row)[18];
+          wf_switch<NPR>(jp, [&](auto Jc) {
+            constexpr int J = decltype(Jc)::value;
+            const uint64_t ONE2 = tc::pk2(1.f, 1.f);
+#pragma unroll
+            for (int w = 0; w < 3; ++w) acc[a][J + w] = tc::fma2(c3[w], ONE2, acc[a][J + w]);
+          });
+        }
+      }
+    }
+    __syncthreads();                              // stage b & 1 and table b & 1 fully read; table (b+1) & 1 complete
     if (threadIdx.x == 0 && b + 2 < nbat) {
       tc::fence_proxy_async_smem();               // generic reads of the stage before the async-proxy refill
       issue(b + 2);

@@ -163,10 +163,11 @@ hrkan_status launch_wgrad_first_r(hrkan_net* net, const float* X0, const float* 
   if (O > FL_THREADS || B > 20 || ((1 + NF + NS) * O * 4) % 16 != 0) return HRKAN_OK;
   auto go = [&](auto BMc) -> hrkan_status {
     constexpr int BMAX = decltype(BMc)::value;
-    auto kfn = k_wgrad_first_r<NF, NS, M, BMAX>;
+    const bool window = HRKAN_WF_WINDOW && net->bc.k <= 3;     // band-limited update (k + 1 <= 4 active bases)
+    auto kfn = window ? k_wgrad_first_w<NF, NS, M, BMAX> : k_wgrad_first_r<NF, NS, M, BMAX>;
     const int pb = wf_pb(1 + NF + NS, O);
-    const size_t ring = std::max<size_t>((size_t)2 * pb * (1 + NF + NS) * O, (size_t)(FL_THREADS / O) * NF * B * O);
-    const size_t smem = sizeof(float) * (ring + (size_t)pb * NF * 3 * BMAX + FL_THREADS);
+    const size_t ring = (std::max<size_t>((size_t)2 * pb * (1 + NF + NS) * O, (size_t)(FL_THREADS / O) * NF * B * O) + 3) & ~(size_t)3;
+    const size_t smem = sizeof(float) * (ring + (window ? (size_t)2 * pb * NF * 20 : (size_t)pb * NF * 3 * BMAX) + FL_THREADS);
     HR_CUDA(smem_optin(kfn, smem));
     int per_sm = 0;
     HR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, FL_THREADS, smem));
@@ -176,7 +177,8 @@ hrkan_status launch_wgrad_first_r(hrkan_net* net, const float* X0, const float* 
     HR_CUDA(net->first_part.ensure(sizeof(float) * (size_t)nzf * (nWf + O)));
     float* fpart = net->first_part.f();
     float* fpart_b = fpart + (size_t)nzf * nWf;
-    HR_LAUNCH(HRKAN_K_WGRAD_FIRST, "k_wgrad_first_r", kfn<<<nzf, FL_THREADS, smem, st>>>(X0, Ybar, fpart, fpart_b, n, O, net->bc));
+    HR_LAUNCH(HRKAN_K_WGRAD_FIRST, window ? "k_wgrad_first_w" : "k_wgrad_first_r",
+              kfn<<<nzf, FL_THREADS, smem, st>>>(X0, Ybar, fpart, fpart_b, n, O, net->bc));
     HR_LAUNCH(HRKAN_K_REDUCE, "k_reduce_parts",
               k_reduce_parts<<<(unsigned)((nWf + O + 255) / 256), 256, 0, st>>>(fpart, fpart_b, nzf, nWf, O, dW, db));
     *done = true;
