@@ -2,6 +2,8 @@
 bench.py for the roofline `traffic` field) and a markdown table.
 
     python scripts/ncu_summary.py report.ncu-rep C5 65536 profiles/r01_ncu_c5   # writes .json and _summary.md
+    python scripts/ncu_summary.py a_raw.csv,b_raw.csv C4 262144 profiles/r02_ncu_c4   # several captures (one kernel
+                                                    # class each, scripts/ncu_classes.sh); units are read per file
 """
 import csv
 import io
@@ -17,12 +19,21 @@ CLASS = [("k_fwd_first", "fwd_first"), ("k_fwd_tc", "fwd_hidden"), ("k_fwd_simt"
 
 
 def main():
-    rep, cfg, npts, out = sys.argv[1], sys.argv[2], int(sys.argv[3]), sys.argv[4]
+    reps, cfg, npts, out = sys.argv[1].split(","), sys.argv[2], int(sys.argv[3]), sys.argv[4]
+    kernels = {}
+    for rep in reps:
+        summarise(rep, npts, kernels)
+    write(cfg, npts, out, kernels)
+
+
+def summarise(rep, npts, kernels):
     if rep.endswith(".csv"):                  # an exported `--page raw --csv` of the report
         txt = open(rep).read()
     else:
         txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(txt)))
+    if len(rows) < 3:
+        return
     hdr = rows[0]
     ix = {h: i for i, h in enumerate(hdr)}
 
@@ -32,7 +43,6 @@ def main():
         except (KeyError, ValueError):
             return None
 
-    kernels = {}
     for r in rows[2:]:
         name = r[ix["Kernel Name"]]
         m = re.search(r"(k_\w+)(<[^>]*>)?", name)
@@ -64,6 +74,9 @@ def main():
         entry["dram_bytes_per_point"] = ((entry["dram_read_bytes"] or 0) + (entry["dram_write_bytes"] or 0)) / npts
         if short not in kernels or kernels[short]["time_ms"] < t_ms:   # keep the interior (largest) launch
             kernels[short] = entry
+
+
+def write(cfg, npts, out, kernels):
     js = {"workload": cfg,
           "capture": f"ncu --set full --clock-control none, scripts/prof_step.py {cfg} {npts} 1 "
                      f"(interior pass, {npts} points, one launch per kernel)",
