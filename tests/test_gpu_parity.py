@@ -38,7 +38,7 @@ def _pde(w):
 
 def _make(w, seed=7, bias_std=0.1, engine=None, chunk=None):
     from paper_2409_14248_b200 import HRKANNet
-    net = HRKANNet(w.widths, w.G, w.k, w.m)
+    net = HRKANNet(w.widths, w.G, w.k, w.m, w.lo, w.hi)
     params = HI.random_params(w.widths, w.G, w.k, seed=seed, bias_std=bias_std)
     net.set_params(HI.flatten_params(params))
     if engine is not None:

@@ -292,6 +292,9 @@ def _stress_cases():
     cases.append((14, 2, 64, 2, 9, 1, 4, "poisson", 1777, 131, 613))
     cases.append((15, 3, 128, 2, 8, 4, 5, "poisson", 1201, 77, 500))
     cases.append((16, 2, 256, 2, 7, 5, 6, "burgers", 999, 64, 1024))
+    # one-dimensional Poisson (D = 1: 3-channel jets, tc_np = 80 points per tile)
+    cases.append((17, 1, 64, 2, 10, 3, 4, "poisson", 1501, 2, 700))
+    cases.append((18, 1, 128, 3, 9, 3, 5, "poisson", 999, 2, 333))
     return cases
 
 
@@ -387,3 +390,23 @@ def test_padded_hidden_widths(torch_mod, widths, pde):
     out2 = _loss_grad_gpu(torch, net, w, ps)
     lp2, lb2, g2 = _loss_grad_oracle(w, HI.unflatten_params(got.astype(np.float64), w.widths, w.B), ps)
     _check_loss_grad(out2, w, lp2, lb2, g2)
+
+
+def test_tensor_core_path_shifted_grid(torch_mod):
+    """A wide net on the paper's transformed Burgers domain (basis grid [0, 2.5], adv 1/4, visc 0.001/16,
+    P:211-224): the tensor-core kernels with grid_lo != -grid_hi and collocation points (and hidden values)
+    partly outside the basis grid."""
+    torch = torch_mod
+    w = HI.Workload("SG", "shifted grid", "burgers", (2, 64, 128, 1), 7, 3, 4, 1800, 150, 90, lo=0.0, hi=2.5,
+                    adv=0.25, visc=0.001 / 16)
+    rng = np.random.default_rng(77)
+    interior = rng.uniform(0.0, 2.5, (w.n_int, 2))
+    interior[::50] += 0.3                               # a few points beyond the grid's upper edge
+    bnd = rng.uniform(0.0, 2.5, (w.n_bnd, 2))
+    bnd[:, 0] = np.where(rng.random(w.n_bnd) < 0.5, 0.0, 2.5)
+    ini = np.stack([np.linspace(0.0, 2.5, w.n_ic), np.zeros(w.n_ic)], axis=1)
+    ps = HI.PointSet(interior.astype(np.float32), bnd.astype(np.float32), np.zeros(w.n_bnd, np.float32),
+                     ini.astype(np.float32), (1.0 / np.cosh(4 * ini[:, 0] - 5)).astype(np.float32))
+    net, params = _make(w, seed=9, chunk=640)
+    out = _loss_grad_gpu(torch, net, w, ps)
+    _check_loss_grad(out, w, *_loss_grad_oracle(w, params, ps))
