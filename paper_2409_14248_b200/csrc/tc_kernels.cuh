@@ -45,6 +45,9 @@ constexpr int TC_GEN_THREADS = 128;   // one generator group (4 warps); the grou
 __host__ __device__ constexpr int tc_ngen(int C, int O) {
   return HRKAN_FWD_NGEN > 0 ? HRKAN_FWD_NGEN : (C == 1 || C == 4 || O <= 64) ? 4 : 3;
 }
+#ifndef HRKAN_FWD_NOCROSS
+#define HRKAN_FWD_NOCROSS 0       // 1: TIMING EXPERIMENT ONLY (wrong results): K chunks never read the next input's jets
+#endif
 #ifndef HRKAN_FWD_SWAP
 #define HRKAN_FWD_SWAP 0          // 1: O = 64 forward with (channel, point) rows on the MMA M side (FwdCfg::SW; measured 12 % slower on C3, off)
 #endif
@@ -299,7 +302,7 @@ __global__ void __launch_bounds__(FwdCfg<NF, NS, M, OO>::THREADS, 1)
         // jets of inputs i0 and i0+1 (the chunk crosses into i0+1 when n0 + 3 >= B)
         float jx[2], jdx[2][NF > 0 ? NF : 1], jddx[2][NS > 0 ? NS : 1];
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
+        for (int h = 0; h < (HRKAN_FWD_NOCROSS ? 1 : 2); ++h) {
           const int i = i0 + h;
           const float* wp = win + ((i / TC_WIN) % TC_NWIN) * Cfg::WIN_FLOATS + (pl * Cfg::CB) * TC_WIN + (i % TC_WIN);
           jx[h] = wp[0];
@@ -319,8 +322,8 @@ __global__ void __launch_bounds__(FwdCfg<NF, NS, M, OO>::THREADS, 1)
 #pragma unroll
           for (int e = 0; e < 4; e += 2) {
             const int na = n0 + e, nb = n0 + e + 1;
-            const bool ha = na >= B, hb = nb >= B;
-            const int nna = ha ? na - B : na, nnb = hb ? nb - B : nb;
+            const bool ha = !HRKAN_FWD_NOCROSS && na >= B, hb = !HRKAN_FWD_NOCROSS && nb >= B;
+            const int nna = ha ? na - B : (HRKAN_FWD_NOCROSS ? min(na, B - 1) : na), nnb = hb ? nb - B : (HRKAN_FWD_NOCROSS ? min(nb, B - 1) : nb);
             const uint64_t qq = tc::fma2(tc::pk2(ha ? jx[1] : jx[0], hb ? jx[1] : jx[0]), SC2, tc::pk2(ncs[nna], ncs[nnb]));
             const uint64_t q2 = tc::mul2(qq, qq);
             float t0, t1;
