@@ -68,6 +68,8 @@ def summarise(rep, npts, kernels):
         entry = {"class": cls, "time_ms": t_ms, "top_stalls": {k: round(100 * v / tot, 1) for k, v in top},
                  "tensor_pipe_pct": val(r, "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed") or 0.0,
                  "issue_active_pct": val(r, "smsp__issue_active.avg.pct_of_peak_sustained_active"),
+                 "fma_pipe_pct": val(r, "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"),
+                 "dram_pct": val(r, "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
                  "lts_pct": val(r, "lts__t_sectors.avg.pct_of_peak_sustained_elapsed"),
                  "dram_read_bytes": rd, "dram_write_bytes": wr,
                  "sm_clock_ghz": val(r, "sm__cycles_elapsed.avg.per_second")}
@@ -83,13 +85,14 @@ def write(cfg, npts, out, kernels):
           "points_per_capture": npts, "kernels": kernels}
     json.dump(js, open(out + ".json", "w"), indent=1)
     lines = [f"# ncu summary, {cfg} (interior pass, {npts} points; `ncu --set full --clock-control none`)", "",
-             "| kernel | time ms | tensor pipe % | issue % | L2 % | DRAM B/point | SM GHz | top stall reasons (% of samples) |",
-             "|---|---|---|---|---|---|---|---|"]
+             "| kernel | time ms | tensor pipe % | FMA pipe % | issue % | L2 % | DRAM % | DRAM B/point | SM GHz | top stall reasons (% of samples) |",
+             "|---|---|---|---|---|---|---|---|---|---|"]
     for k, e in sorted(kernels.items(), key=lambda kv: -kv[1]["time_ms"]):
         if e["time_ms"] < 0.005:
             continue
-        lines.append(f"| `{k}` | {e['time_ms']:.3f} | {e['tensor_pipe_pct']:.1f} | {e['issue_active_pct'] or 0:.1f} | "
-                     f"{e['lts_pct'] or 0:.1f} | {e['dram_bytes_per_point']:.0f} | {e['sm_clock_ghz'] or 0:.2f} | "
+        lines.append(f"| `{k}` | {e['time_ms']:.3f} | {e['tensor_pipe_pct']:.1f} | {e.get('fma_pipe_pct') or 0:.1f} | "
+                     f"{e['issue_active_pct'] or 0:.1f} | {e['lts_pct'] or 0:.1f} | {e.get('dram_pct') or 0:.1f} | "
+                     f"{e['dram_bytes_per_point']:.0f} | {e['sm_clock_ghz'] or 0:.2f} | "
                      + ", ".join(f"{k} {v}" for k, v in e.get("top_stalls", {}).items()) + " |")
     open(out + "_summary.md", "w").write("\n".join(lines) + "\n")
     print("\n".join(lines))
