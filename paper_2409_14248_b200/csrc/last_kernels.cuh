@@ -27,7 +27,7 @@ using namespace hrkan;
 
 constexpr int LF_WARPS = 4;
 
-// Output-layer basis arithmetic on packed fp32 pairs (two bases per FFMA2/FMUL2): v0..v3 of
+// Output-layer basis arithmetic on packed fp32 pairs (two bases per FFMA2/FMUL2, m >= 4): v0..v3 of
 // bases na, nb at x with t = 1 - q^2 clamped at 0 (NaN kept), zero where !ok (outside [0, B)).
 #ifndef HRKAN_LAST_F32X2
 #define HRKAN_LAST_F32X2 1
@@ -45,26 +45,15 @@ __device__ __forceinline__ void hr_eval_pair(float x, int na, int nb, bool oka, 
   t0 = oka ? max_nan(t0, 0.f) : 0.f;
   t1 = okb ? max_nan(t1, 0.f) : 0.f;
   const uint64_t t = pk2(t0, t1);
-  // t^(m-3), t^(m-2): products for m >= 4; for m = 3 and m = 2 the zeroth power is the support mask
-  uint64_t tm3, tm2;
-  if constexpr (M >= 4) {
-    tm3 = ONE2;
+  uint64_t tm3 = ONE2;
 #pragma unroll
-    for (int e = 0; e < M - 3; ++e) tm3 = mul2(tm3, t);
-    tm2 = mul2(tm3, t);
-  } else if constexpr (M == 3) {
-    tm3 = pos_mask2(t0, t1);
-    tm2 = t;
-  } else {
-    tm3 = tm2 = pos_mask2(t0, t1);
-  }
-  const uint64_t tm1 = mul2(tm2, t);
+  for (int e = 0; e < M - 3; ++e) tm3 = mul2(tm3, t);
+  const uint64_t tm2 = mul2(tm3, t), tm1 = mul2(tm2, t);
   v0 = mul2(tm1, t);
   const float c1 = -2.f * M * sc, c2 = c1 * sc, c3 = 4.f * M * (M - 1) * sc * sc * sc;
   v1 = mul2(mul2(qq, tm1), pk2(c1, c1));
   v2 = mul2(mul2(tm2, fma2(q2, K22, ONE2)), pk2(c2, c2));
-  if constexpr (M == 2) v3 = mul2(mul2(qq, tm3), pk2(24.f * sc * sc * sc, 24.f * sc * sc * sc));   // 24 q sc^3 inside the support
-  else v3 = mul2(mul2(mul2(qq, tm3), fma2(q2, K22, pk2(3.f, 3.f))), pk2(c3, c3));
+  v3 = mul2(mul2(mul2(qq, tm3), fma2(q2, K22, pk2(3.f, 3.f))), pk2(c3, c3));
 }
 enum LastMode { LAST_JET = 0, LAST_POISSON = 1, LAST_BURGERS = 2, LAST_BOUNDARY = 3 };
 

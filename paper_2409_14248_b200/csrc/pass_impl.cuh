@@ -23,7 +23,7 @@ hrkan_status launch_last(hrkan_net* net, const float* in, int64_t n, const PassA
   const int I = net->widths[l];
   const int IB = I * net->B;
   constexpr int C = 1 + NF + NS;
-  if constexpr (!FIRST && MODE != LAST_JET) {
+  if constexpr (!FIRST && MODE != LAST_JET && M >= 4) {
     if (I % 32 == 0 && I <= 256 && net->bc.k + 1 <= LV3_KT) {
       // input-parallel, bulk-copied jet batches, cached basis values (k_last_v3)
       constexpr bool CAN_SPLIT = tc_np(C) > 0;

@@ -211,7 +211,7 @@ __global__ void __launch_bounds__(DgrCfg<NF, NS, M, OO>::THREADS, 1)
           for (int a = 0; a < NS; ++a) ddxb[a] = 0.f;
           const float* Sp = S + (pq * C) * DGR_SST + (i * B - row0);   // row of basis n: i*B + n - row0
 #if HRKAN_DGR_F32X2
-          if constexpr (M >= 2) {
+          if constexpr (M >= 4) {
             // two bases per instruction (FFMA2/FMUL2); t clamped at 0 (NaN kept) zeroes v1..v3 outside
             // the support and for bases outside this tile (m >= 4); their smem rows are clamped in range
             const uint64_t ONE2 = tc::pk2(1.f, 1.f), NEG2 = tc::pk2(-1.f, -1.f);
@@ -239,25 +239,14 @@ __global__ void __launch_bounds__(DgrCfg<NF, NS, M, OO>::THREADS, 1)
               t0 = oka ? tc::max_nan(t0, 0.f) : 0.f;
               t1 = okb ? tc::max_nan(t1, 0.f) : 0.f;
               const uint64_t t = tc::pk2(t0, t1);
-              // t^(m-3), t^(m-2): products for m >= 4; for m = 3 and m = 2 the zeroth power is the support mask
-              uint64_t tm3, tm2;
-              if constexpr (M >= 4) {
-                tm3 = ONE2;
+              uint64_t tm3 = ONE2;
 #pragma unroll
-                for (int e = 0; e < M - 3; ++e) tm3 = tc::mul2(tm3, t);
-                tm2 = tc::mul2(tm3, t);
-              } else if constexpr (M == 3) {
-                tm3 = tc::pos_mask2(t0, t1);
-                tm2 = t;
-              } else {
-                tm3 = tm2 = tc::pos_mask2(t0, t1);
-              }
-              const uint64_t tm1 = tc::mul2(tm2, t);
+              for (int e = 0; e < M - 3; ++e) tm3 = tc::mul2(tm3, t);
+              const uint64_t tm2 = tc::mul2(tm3, t), tm1 = tc::mul2(tm2, t);
               const uint64_t v1 = tc::mul2(tc::mul2(qq, tm1), C12);
               const uint64_t kq = tc::fma2(q2, K22, ONE2);                      // 1 - (2m-1) q^2
               const uint64_t v2 = tc::mul2(tc::mul2(tm2, kq), C22);
-              const uint64_t v3 = (M == 2) ? tc::mul2(tc::mul2(qq, tm3), tc::pk2(24.f * sc * sc * sc, 24.f * sc * sc * sc))
-                                           : tc::mul2(tc::mul2(tc::mul2(qq, tm3), tc::fma2(q2, K22, THREE2)), C32);
+              const uint64_t v3 = tc::mul2(tc::mul2(tc::mul2(qq, tm3), tc::fma2(q2, K22, THREE2)), C32);
               uint64_t ab[C];
 #pragma unroll
               for (int c = 0; c < C; ++c) ab[c] = tc::pk2(Sp[c * DGR_SST + ca], Sp[c * DGR_SST + cb]);

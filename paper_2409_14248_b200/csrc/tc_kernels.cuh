@@ -313,7 +313,7 @@ __global__ void __launch_bounds__(FwdCfg<NF, NS, M, OO>::THREADS, 1)
         }
         float va[C][4];
 #if HRKAN_FWD_F32X2
-        if constexpr (M >= 2) {
+        if constexpr (M >= 3) {
           // two K slots per instruction (FFMA2/FMUL2); same formulas as hr_eval with t clamped at 0
           // (NaN kept), so every derivative vanishes outside the support (m >= 3)
           const uint64_t SC2 = tc::pk2(bc.sc, bc.sc), ONE2 = tc::pk2(1.f, 1.f), NEG2 = tc::pk2(-1.f, -1.f);
@@ -331,7 +331,7 @@ __global__ void __launch_bounds__(FwdCfg<NF, NS, M, OO>::THREADS, 1)
             t0 = (i0 * B + na < K) ? tc::max_nan(t0, 0.f) : 0.f;
             t1 = (i0 * B + nb < K) ? tc::max_nan(t1, 0.f) : 0.f;
             const uint64_t t = tc::pk2(t0, t1);
-            uint64_t tm2 = (M == 2) ? tc::pos_mask2(t0, t1) : ONE2;   // t^(m-2); m = 2: the support mask (t^0)
+            uint64_t tm2 = ONE2;
 #pragma unroll
             for (int k = 0; k < M - 2; ++k) tm2 = tc::mul2(tm2, t);
             const uint64_t tm1 = tc::mul2(tm2, t);

@@ -132,13 +132,6 @@ __device__ __forceinline__ float max_nan(float a, float b) {   // NaN-propagatin
   return d;
 }
 
-// Support mask of a clamped t = max(1 - q^2, 0) pair: 1 where t > 0, else 0 (a NaN t gives 0, and NaN * 0 stays
-// NaN downstream).  The packed-pair basis code multiplies by it the derivatives that do not vanish with t: the
-// second derivative for m = 2 and the third for m = 2, 3 carry t^0 (hr_basis.cuh; strict interior, DESIGN reading 2).
-__device__ __forceinline__ uint64_t pos_mask2(float t0, float t1) {
-  return pk2(t0 > 0.f ? 1.f : 0.f, t1 > 0.f ? 1.f : 0.f);
-}
-
 // generic-proxy smem writes -> visible to the async proxy (tensor core / bulk copy)
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
